@@ -1,0 +1,197 @@
+// TEST INFRASTRUCTURE ONLY — C entry points over the UNMODIFIED reference
+// library (/root/reference/proj/src, compiled in place by oracle/Makefile into
+// oracle/_ref/libanchorref.so).  Used to (1) generate the golden fixtures that
+// pin the plain-C restatement (oracle/anchor_oracle.c) and (2) time the
+// reference CPU path in bench.py's reference arm / cpu_baseline.
+//
+// Every call goes through the reference's own public API:
+//   compute_anchor          R/include/anchorattn/anchor_pass.hpp:37
+//   identify_stripes[_zero] R/include/anchorattn/stripe_identify.hpp:44-49
+//   sparse_attention        R/include/anchorattn/sparse_exec.hpp:35-37
+//   anchor_attention        R/include/anchorattn/sparse_exec.hpp:42-43
+//   parallel_for            R/include/anchorattn/parallel.hpp:12-16
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "anchorattn/anchor_pass.hpp"
+#include "anchorattn/metrics.hpp"
+#include "anchorattn/oracle.hpp"
+#include "anchorattn/parallel.hpp"
+#include "anchorattn/sparse_exec.hpp"
+#include "anchorattn/stripe_identify.hpp"
+#include "anchorattn/workloads.hpp"
+
+using namespace anchorattn;
+
+namespace {
+
+thread_local std::string g_err;
+
+Matrix mat(const float* p, std::int64_t rows, std::int64_t cols) {
+    Matrix m(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols));
+    std::memcpy(m.data.data(), p, m.data.size() * sizeof(float));
+    return m;
+}
+
+BlockConfig cfg_of(std::int64_t b_q, std::int64_t b_kv, std::int64_t step, double theta) {
+    BlockConfig c;
+    c.b_q = static_cast<std::size_t>(b_q);
+    c.b_kv = static_cast<std::size_t>(b_kv);
+    c.step = static_cast<std::size_t>(step);
+    c.theta = theta;
+    return c;
+}
+
+// Group g's slot base in the capacity layout used by the oracle and the GPU ABI.
+std::size_t stripe_offset(std::size_t g, const BlockConfig& c, std::size_t n) {
+    std::size_t off = 0;
+    for (std::size_t h = 0; h < g; ++h) {
+        const std::size_t e = middle_end_token(h, c, n);
+        off += e > c.b_kv ? e - c.b_kv : 0;
+    }
+    return off;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// One head through compute_anchor -> identify_stripes -> sparse_attention,
+// exposing every intermediate.  Returns 0 on success, 1 on exception.
+int ref_pipeline(std::int64_t n, std::int64_t d, const float* q, const float* k, const float* v,
+                 std::int64_t b_q, std::int64_t b_kv, std::int64_t step, double theta,
+                 int zero_anchor, float* out, double* m, double* l, double* acc,
+                 float* anchor_out_f /*finalize_anchor*/, double* pooled_anchor_out,
+                 std::uint32_t* idx, std::int64_t* counts, std::int64_t* computed) {
+    try {
+        const HeadWorkload w = HeadWorkload::create(mat(q, n, d), mat(k, n, d), mat(v, n, d));
+        const BlockConfig cfg = cfg_of(b_q, b_kv, step, theta);
+        const AnchorState st = compute_anchor(w, cfg);
+        const StripeIndex si =
+            zero_anchor ? identify_stripes_zero_anchor(w, cfg) : identify_stripes(w, st, cfg);
+        const SparseResult res = sparse_attention(w, st, si, cfg);
+        std::memcpy(out, res.out.o.data.data(), static_cast<std::size_t>(n * d) * sizeof(float));
+        if (m) std::memcpy(m, st.m.data(), st.m.size() * sizeof(double));
+        if (l) std::memcpy(l, st.l.data(), st.l.size() * sizeof(double));
+        if (acc) std::memcpy(acc, st.acc.data(), st.acc.size() * sizeof(double));
+        if (anchor_out_f) {
+            const AttentionOutput fa = finalize_anchor(st);
+            std::memcpy(anchor_out_f, fa.o.data.data(), fa.o.data.size() * sizeof(float));
+        }
+        if (pooled_anchor_out) {
+            const auto pa = pooled_anchor(st, cfg);
+            std::memcpy(pooled_anchor_out, pa.data(), pa.size() * sizeof(double));
+        }
+        for (std::size_t g = 0; g < si.groups.size(); ++g) {
+            const std::size_t off = stripe_offset(g, cfg, static_cast<std::size_t>(n));
+            if (idx)
+                std::memcpy(idx + off, si.groups[g].data(), si.groups[g].size() * 4);
+            if (counts) counts[g] = static_cast<std::int64_t>(si.groups[g].size());
+        }
+        if (computed) *computed = static_cast<std::int64_t>(res.stats.computed_positions);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// A layer of `heads` independent heads (GQA: Q head h reads KV head
+// h / (heads / kv_heads)), each through anchor_attention, spread over the
+// reference's own parallel_for.  Layouts: q [heads, n, d], k/v [kv_heads, n, d].
+int ref_layer(std::int64_t heads, std::int64_t kv_heads, std::int64_t n, std::int64_t d,
+              const float* q, const float* k, const float* v, std::int64_t b_q,
+              std::int64_t b_kv, std::int64_t step, double theta, int zero_anchor, float* out,
+              std::int64_t* computed) {
+    try {
+        const BlockConfig cfg = cfg_of(b_q, b_kv, step, theta);
+        const std::int64_t per = heads / kv_heads;
+        const std::size_t hd = static_cast<std::size_t>(n * d);
+        parallel_for(static_cast<std::size_t>(heads), [&](std::size_t h) {
+            const std::size_t kvh = h / static_cast<std::size_t>(per);
+            const HeadWorkload w = HeadWorkload::create(
+                mat(q + h * hd, n, d), mat(k + kvh * hd, n, d), mat(v + kvh * hd, n, d));
+            const SparseResult res = anchor_attention(w, cfg, zero_anchor != 0);
+            std::memcpy(out + h * hd, res.out.o.data.data(), hd * sizeof(float));
+            computed[h] = static_cast<std::int64_t>(res.stats.computed_positions);
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+int ref_dense_attention(std::int64_t n, std::int64_t d, const float* q, const float* k,
+                        const float* v, float* out) {
+    try {
+        const HeadWorkload w = HeadWorkload::create(mat(q, n, d), mat(k, n, d), mat(v, n, d));
+        const AttentionOutput o = dense_attention(w);
+        std::memcpy(out, o.o.data.data(), o.o.data.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// recall(union_mask(identify_stripes(...)), dense_probs(q, k)) — the
+// reference's own recall measurement (R/src/metrics.cpp:8-19).
+int ref_recall(std::int64_t n, std::int64_t d, const float* q, const float* k, const float* v,
+               std::int64_t b_q, std::int64_t b_kv, std::int64_t step, double theta,
+               int zero_anchor, double* recall_out, double* sparsity_out) {
+    try {
+        const HeadWorkload w = HeadWorkload::create(mat(q, n, d), mat(k, n, d), mat(v, n, d));
+        const BlockConfig cfg = cfg_of(b_q, b_kv, step, theta);
+        const AnchorState st = compute_anchor(w, cfg);
+        const StripeIndex si =
+            zero_anchor ? identify_stripes_zero_anchor(w, cfg) : identify_stripes(w, st, cfg);
+        const SelectionMask mask = union_mask(si, cfg, static_cast<std::size_t>(n));
+        *recall_out = recall(mask, dense_probs(w.q, w.k));
+        *sparsity_out = sparsity(mask);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// Reference generators, for building fixtures (workloads.hpp:12-38).
+int ref_gen_random(std::int64_t n, std::int64_t d, std::uint64_t seed, float* q, float* k,
+                   float* v) {
+    try {
+        const auto heads = gen_random(static_cast<std::size_t>(n), static_cast<std::size_t>(d), 1,
+                                      seed);
+        std::memcpy(q, heads[0].q.data.data(), static_cast<std::size_t>(n * d) * 4);
+        std::memcpy(k, heads[0].k.data.data(), static_cast<std::size_t>(n * d) * 4);
+        std::memcpy(v, heads[0].v.data.data(), static_cast<std::size_t>(n * d) * 4);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+int ref_gen_sink_local(std::int64_t n, std::int64_t d, double sink_strength,
+                       std::int64_t window, std::uint64_t seed, float* q, float* k, float* v) {
+    try {
+        const HeadWorkload w = gen_sink_local(static_cast<std::size_t>(n),
+                                              static_cast<std::size_t>(d), sink_strength,
+                                              static_cast<std::size_t>(window), seed);
+        std::memcpy(q, w.q.data.data(), static_cast<std::size_t>(n * d) * 4);
+        std::memcpy(k, w.k.data.data(), static_cast<std::size_t>(n * d) * 4);
+        std::memcpy(v, w.v.data.data(), static_cast<std::size_t>(n * d) * 4);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+std::int64_t ref_max_threads() { return static_cast<std::int64_t>(max_threads()); }
+
+}  // extern "C"
