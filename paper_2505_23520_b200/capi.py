@@ -1,0 +1,293 @@
+"""ctypes binding of the C ABI (include/anchorattn_capi.h) for device tensors.
+
+This is the batched, device-resident entry used by bench.py and the GPU
+tests: torch supplies device memory and the stream (plumbing only); every
+computation runs in ``lib/libanchorattn_b200.so``.  Loading fails loudly when
+the library is missing — there is no Python or CPU fallback.
+
+Tensor layouts (head-major, contiguous): q [hq, n, d], k / v [hkv, n, d].
+dtype torch.bfloat16 selects the tcgen05 path, torch.float32 the exact path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libanchorattn_b200.so")
+
+AA_F32, AA_BF16, AA_F64 = 0, 1, 2
+_STATUS = {0: "AA_OK", 1: "AA_ERR_INVALID_ARGUMENT", 2: "AA_ERR_OUT_OF_RANGE",
+           3: "AA_ERR_UNSUPPORTED", 4: "AA_ERR_CUDA"}
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("b_q", C.c_int64), ("b_kv", C.c_int64), ("step", C.c_int64),
+                ("theta", C.c_double)]
+
+
+class _Problem(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int64), ("hq", C.c_int64), ("hkv", C.c_int64),
+                ("cfg", _Cfg), ("dtype", C.c_int), ("q_row_stride", C.c_int64),
+                ("q_head_stride", C.c_int64), ("kv_row_stride", C.c_int64),
+                ("kv_head_stride", C.c_int64)]
+
+
+class _Plan(C.Structure):
+    _fields_ = [("q_blocks", C.c_int64), ("groups", C.c_int64), ("state_dtype", C.c_int),
+                ("stripe_capacity", C.c_int64), ("covered_positions", C.c_int64),
+                ("workspace_bytes", C.c_size_t)]
+
+
+class AnchorAttnError(RuntimeError):
+    pass
+
+
+class InvalidArgument(AnchorAttnError, ValueError):
+    pass
+
+
+class OutOfRange(AnchorAttnError, IndexError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load the native library (builds it first when sources are newer)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_2505_23520_b200/build.py "
+                              "(anchorattn has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.aa_last_error.restype = C.c_char_p
+        L.aa_version.restype = C.c_char_p
+        p = C.c_void_p
+        P = C.POINTER(_Problem)
+        sigs = {
+            "aa_make_plan": [P, C.POINTER(_Plan)],
+            "aa_compute_anchor": [P, p, p, p, p, p, p, p, p, p],
+            "aa_pool": [P, p, p, p, p, p, p, p],
+            "aa_identify": [P, p, p, p, C.c_int, p, p, p, C.c_size_t, p],
+            "aa_sparse_attention": [P, p, p, p, p, p, p, p, p, p, C.c_int64, p, C.c_int, p, p],
+            "aa_finalize_anchor": [P, p, p, p, C.c_int, p],
+            "aa_anchor_attention": [P, p, p, p, C.c_int, p, C.c_int, p, p, C.c_size_t, p],
+            "aa_anchor_attention_host": [P, p, p, p, C.c_int, p, C.c_int, p],
+            "aa_dense_attention": [P, p, p, p, p, C.c_int, p],
+            "aa_union_recall": [P, p, p, p, p, p, p],
+            "aa_stream_sync": [p],
+        }
+        for name, args in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        for name in ("aa_group_count", "aa_anchor_covered_count"):
+            getattr(L, name).restype = C.c_int64
+            getattr(L, name).argtypes = [C.c_int64, C.POINTER(_Cfg)]
+        for name in ("aa_window_start_token", "aa_middle_end_token", "aa_stripe_offset"):
+            getattr(L, name).restype = C.c_int64
+            getattr(L, name).argtypes = [C.c_int64, C.POINTER(_Cfg), C.c_int64]
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    msg = lib().aa_last_error().decode()
+    if status == 1:
+        raise InvalidArgument(msg)
+    if status == 2:
+        raise OutOfRange(msg)
+    raise AnchorAttnError(f"{_STATUS.get(status, status)}: {msg}")
+
+
+@dataclass(frozen=True)
+class BlockConfig:
+    """BlockConfig (R/include/anchorattn/matrix.hpp:53-62), paper defaults."""
+
+    b_q: int = 128
+    b_kv: int = 128
+    step: int = 16
+    theta: float = 12.0
+
+    def c(self) -> _Cfg:
+        return _Cfg(self.b_q, self.b_kv, self.step, float(self.theta))
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return AA_BF16
+    if t.dtype == torch.float32:
+        return AA_F32
+    raise TypeError(f"q/k/v must be bfloat16 (fast path) or float32 (exact path), got {t.dtype}")
+
+
+def make_problem(q: torch.Tensor, k: torch.Tensor, cfg: BlockConfig) -> _Problem:
+    if q.dim() != 3 or k.dim() != 3:
+        raise ValueError("expected q [hq, n, d] and k/v [hkv, n, d]")
+    hq, n, d = q.shape
+    hkv = k.shape[0]
+    if k.shape[1:] != (n, d):
+        raise ValueError("q and k/v must share (n, d)")
+    if q.stride(2) != 1 or k.stride(2) != 1:
+        raise ValueError("head dim must be contiguous")
+    return _Problem(n, d, hq, hkv, cfg.c(), _dtype_code(q), q.stride(1), q.stride(0),
+                    k.stride(1), k.stride(0))
+
+
+def plan(p: _Problem) -> _Plan:
+    pl = _Plan()
+    _check(lib().aa_make_plan(C.byref(p), C.byref(pl)))
+    return pl
+
+
+def stripe_offsets(n: int, cfg: BlockConfig) -> list:
+    c = cfg.c()
+    G = lib().aa_group_count(n, C.byref(c))
+    return [lib().aa_stripe_offset(g, C.byref(c), n) for g in range(G + 1)]
+
+
+def _out_code(dt):
+    return AA_BF16 if dt == torch.bfloat16 else AA_F32
+
+
+class Pipeline:
+    """Reusable device workspace for repeated calls on one problem shape."""
+
+    def __init__(self, q, k, v, cfg: BlockConfig):
+        self.cfg = cfg
+        self.p = make_problem(q, k, cfg)
+        self.plan = plan(self.p)
+        self.workspace = torch.empty(self.plan.workspace_bytes, dtype=torch.uint8, device=q.device)
+
+    def __call__(self, q, k, v, zero_anchor=False, out=None, out_dtype=torch.float32,
+                 computed=None):
+        hq, n, d = q.shape
+        if out is None:
+            out = torch.empty((hq, n, d), dtype=out_dtype, device=q.device)
+        if computed is None:
+            computed = torch.empty(hq, dtype=torch.int64, device=q.device)
+        _check(lib().aa_anchor_attention(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v),
+                                         int(zero_anchor), _ptr(out), _out_code(out.dtype),
+                                         _ptr(computed), _ptr(self.workspace),
+                                         self.plan.workspace_bytes, _stream()))
+        return out, computed
+
+
+def anchor_attention(q, k, v, cfg=BlockConfig(), zero_anchor=False, out_dtype=torch.float32):
+    """anchor_attention (R/src/sparse_exec.cpp:126-133) over all heads.
+
+    Returns (out [hq, n, d], computed_positions [hq] int64)."""
+    return Pipeline(q, k, v, cfg)(q, k, v, zero_anchor=zero_anchor, out_dtype=out_dtype)
+
+
+def compute_anchor(q, k, v, cfg=BlockConfig()):
+    """Alg. 1: returns dict(m, l, acc, qsum, msum) (state f64 on the exact path)."""
+    p = make_problem(q, k, cfg)
+    pl = plan(p)
+    hq, n, d = q.shape
+    sdt = torch.float64 if pl.state_dtype == AA_F64 else torch.float32
+    m = torch.empty((hq, n), dtype=sdt, device=q.device)
+    l = torch.empty_like(m)
+    acc = torch.empty((hq, n, d), dtype=sdt, device=q.device)
+    qsum = torch.empty((hq, pl.q_blocks, d), dtype=torch.float32, device=q.device)
+    msum = torch.empty((hq, pl.q_blocks), dtype=torch.float64, device=q.device)
+    fast = p.dtype == AA_BF16
+    _check(lib().aa_compute_anchor(C.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(l),
+                                   _ptr(acc), _ptr(qsum) if fast else None,
+                                   _ptr(msum) if fast else None, _stream()))
+    return dict(m=m, l=l, acc=acc, qsum=qsum if fast else None, msum=msum if fast else None)
+
+
+def pool(q, k, state, cfg=BlockConfig(), use_partials=True):
+    """pooled_anchor + avgpool_rows(Q): returns (anchor [hq, G] f64, qbar [hq, G, d] f32)."""
+    p = make_problem(q, k, cfg)
+    pl = plan(p)
+    hq, n, d = q.shape
+    anchor = torch.empty((hq, pl.groups), dtype=torch.float64, device=q.device)
+    qbar = torch.empty((hq, pl.groups, d), dtype=torch.float32, device=q.device)
+    qsum = state.get("qsum") if use_partials else None
+    msum = state.get("msum") if use_partials else None
+    _check(lib().aa_pool(C.byref(p), _ptr(q), _ptr(state["m"]), _ptr(qsum), _ptr(msum),
+                         _ptr(anchor), _ptr(qbar), _stream()))
+    return anchor, qbar
+
+
+def identify(q, k, qbar, anchor, cfg=BlockConfig(), zero_anchor=False):
+    """Alg. 2: returns (indices [hq, capacity] u32-as-int32, counts [hq, G] int32)."""
+    p = make_problem(q, k, cfg)
+    pl = plan(p)
+    hq = q.shape[0]
+    cap = max(pl.stripe_capacity, 1)
+    idx = torch.zeros((hq, cap), dtype=torch.int32, device=q.device)
+    counts = torch.zeros((hq, pl.groups), dtype=torch.int32, device=q.device)
+    _check(lib().aa_identify(C.byref(p), _ptr(k), _ptr(qbar), _ptr(anchor), int(zero_anchor),
+                             _ptr(idx), _ptr(counts), None, 0, _stream()))
+    return idx, counts
+
+
+def sparse(q, k, v, state, idx, counts, cfg=BlockConfig(), offsets=None, fold_chunk=64,
+           out_dtype=torch.float32):
+    """Alg. 3: returns (out [hq, n, d], computed [hq])."""
+    p = make_problem(q, k, cfg)
+    hq, n, d = q.shape
+    out = torch.empty((hq, n, d), dtype=out_dtype, device=q.device)
+    computed = torch.empty(hq, dtype=torch.int64, device=q.device)
+    _check(lib().aa_sparse_attention(C.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(state["m"]),
+                                     _ptr(state["l"]), _ptr(state["acc"]), _ptr(idx),
+                                     _ptr(counts), _ptr(offsets), fold_chunk, _ptr(out),
+                                     _out_code(out_dtype), _ptr(computed), _stream()))
+    return out, computed
+
+
+def finalize(q, k, state, cfg=BlockConfig(), out_dtype=torch.float32):
+    p = make_problem(q, k, cfg)
+    out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    _check(lib().aa_finalize_anchor(C.byref(p), _ptr(state["l"]), _ptr(state["acc"]), _ptr(out),
+                                    _out_code(out_dtype), _stream()))
+    return out
+
+
+def dense_attention(q, k, v, out_dtype=torch.float32, out=None):
+    """Dense causal attention (the baseline; exact or tcgen05 by dtype)."""
+    p = make_problem(q, k, BlockConfig())
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    _check(lib().aa_dense_attention(C.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                    _out_code(out.dtype), _stream()))
+    return out
+
+
+def union_recall(q, k, idx, counts, cfg=BlockConfig()):
+    """Per-head recall of covered ∪ stripes under dense softmax (metrics.cpp:8-19)."""
+    p = make_problem(q, k, cfg)
+    r = torch.empty(q.shape[0], dtype=torch.float64, device=q.device)
+    _check(lib().aa_union_recall(C.byref(p), _ptr(q), _ptr(k), _ptr(idx), _ptr(counts), _ptr(r),
+                                 _stream()))
+    return r
+
+
+def anchor_attention_host(q, k, v, cfg=BlockConfig(), zero_anchor=False,
+                          out_dtype=torch.float32):
+    """The chain on HOST (pinned) tensors through aa_anchor_attention_host."""
+    p = make_problem(q, k, cfg)
+    out = torch.empty(q.shape, dtype=out_dtype, pin_memory=q.is_pinned())
+    computed = torch.empty(q.shape[0], dtype=torch.int64)
+    _check(lib().aa_anchor_attention_host(C.byref(p), _ptr(q), _ptr(k), _ptr(v),
+                                          int(zero_anchor), _ptr(out), _out_code(out_dtype),
+                                          _ptr(computed)))
+    return out, computed

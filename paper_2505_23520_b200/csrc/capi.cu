@@ -1,0 +1,565 @@
+// C ABI implementation (include/anchorattn_capi.h): validation with the
+// reference's exception texts, path dispatch, workspace carving and the
+// host-buffer entry point.  No computation happens on the host: every entry
+// that produces values launches CUDA kernels and fails with AA_ERR_CUDA when
+// no device is present.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/anchorattn_capi.h"
+#include "common.cuh"
+#include "fast.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+aa_status fail(aa_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+aa_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(AA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define AA_CUDA(call)                                                  \
+    do {                                                               \
+        cudaError_t e_ = (call);                                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);            \
+    } while (0)
+
+aa::Geo geo_of(int64_t n, const aa_block_config& c) { return aa::Geo{n, c.b_q, c.b_kv, c.step}; }
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Buffers of the fused chain, carved from one workspace.
+struct Carve {
+    size_t off = 0;
+    char* base = nullptr;
+    void* take(size_t bytes) {
+        void* p = base ? base + off : nullptr;
+        off += align256(bytes);
+        return p;
+    }
+};
+
+struct Layout {
+    void *m, *l, *acc, *qsum, *msum, *anchor, *qbar, *offsets, *bits, *indices, *counts, *taken,
+        *v16;
+    int64_t words_per_row;
+    size_t total;
+};
+
+Layout carve(const aa_problem& p, const aa_plan& plan, void* ws) {
+    Carve c;
+    c.base = static_cast<char*>(ws);
+    Layout L{};
+    const size_t se = plan.state_dtype == AA_F64 ? 8 : 4;
+    const size_t hq = static_cast<size_t>(p.hq), n = static_cast<size_t>(p.n),
+                 d = static_cast<size_t>(p.d), G = static_cast<size_t>(plan.groups),
+                 T = static_cast<size_t>(plan.q_blocks);
+    L.words_per_row = (p.n + 31) / 32;
+    L.m = c.take(hq * n * se);
+    L.l = c.take(hq * n * se);
+    L.acc = c.take(hq * n * d * se);
+    L.qsum = c.take(hq * T * d * 4);
+    L.msum = c.take(hq * T * 8);
+    L.anchor = c.take(hq * G * 8);
+    L.qbar = c.take(hq * G * d * 4);
+    L.offsets = c.take((G + 1) * 8);
+    L.bits = c.take(hq * G * static_cast<size_t>(L.words_per_row) * 4);
+    L.indices = c.take(hq * static_cast<size_t>(plan.stripe_capacity > 0 ? plan.stripe_capacity : 1) * 4);
+    L.counts = c.take(hq * G * 4);
+    L.taken = c.take(hq * 8);
+    L.v16 = p.dtype == AA_BF16 ? c.take(static_cast<size_t>(p.hkv) * n * d * 2) : nullptr;
+    L.total = c.off;
+    return L;
+}
+
+aa::ExactArgs exact_args(const aa_problem& p) {
+    aa::ExactArgs a{};
+    a.geo = geo_of(p.n, p.cfg);
+    a.d = p.d;
+    a.hq = p.hq;
+    a.hkv = p.hkv;
+    a.rep = p.hq / p.hkv;
+    a.q_rs = p.q_row_stride ? p.q_row_stride : p.d;
+    a.q_hs = p.q_head_stride ? p.q_head_stride : p.n * a.q_rs;
+    a.kv_rs = p.kv_row_stride ? p.kv_row_stride : p.d;
+    a.kv_hs = p.kv_head_stride ? p.kv_head_stride : p.n * a.kv_rs;
+    a.inv_sqrt_d = 1.0 / std::sqrt(static_cast<double>(p.d));
+    a.theta = p.cfg.theta;
+    return a;
+}
+
+aa::FastArgs fast_args(const aa_problem& p) {
+    aa::FastArgs f{};
+    f.geo = geo_of(p.n, p.cfg);
+    f.hq = p.hq;
+    f.hkv = p.hkv;
+    f.rep = p.hq / p.hkv;
+    f.q_rs = p.q_row_stride ? p.q_row_stride : p.d;
+    f.q_hs = p.q_head_stride ? p.q_head_stride : p.n * f.q_rs;
+    f.kv_rs = p.kv_row_stride ? p.kv_row_stride : p.d;
+    f.kv_hs = p.kv_head_stride ? p.kv_head_stride : p.n * f.kv_rs;
+    f.theta = p.cfg.theta;
+    return f;
+}
+
+// Stream-ordered temporary (cudaMallocAsync pool) freed on scope exit.
+struct Temp {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit Temp(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 1, s); }
+    ~Temp() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+aa_status require_device() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(AA_ERR_CUDA, std::string("no CUDA device available (") +
+                                     cudaGetErrorString(e) +
+                                     "); anchorattn has no CPU fallback");
+    return AA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* aa_last_error(void) { return g_err.c_str(); }
+const char* aa_version(void) { return "anchorattn-b200 0.1 (sm_100a)"; }
+
+aa_status aa_config_validate(const aa_block_config* c) {
+    if (!c) return fail(AA_ERR_INVALID_ARGUMENT, "BlockConfig: null");
+    // R/src/matrix.cpp:31-42
+    if (c->b_q <= 0 || c->b_kv <= 0 || c->step <= 0)
+        return fail(AA_ERR_INVALID_ARGUMENT, "BlockConfig: b_q, b_kv, step must be >= 1");
+    if (c->b_q % c->b_kv != 0 && c->b_kv % c->b_q != 0)
+        return fail(AA_ERR_INVALID_ARGUMENT,
+                    "BlockConfig: one of b_q, b_kv must divide the other");
+    if (!std::isfinite(c->theta))
+        return fail(AA_ERR_INVALID_ARGUMENT, "BlockConfig: theta must be finite");
+    return AA_OK;
+}
+
+int64_t aa_group_count(int64_t n, const aa_block_config* c) { return geo_of(n, *c).groups(); }
+int64_t aa_window_start_token(int64_t g, const aa_block_config* c, int64_t n) {
+    return geo_of(n, *c).window_start(g);
+}
+int64_t aa_middle_end_token(int64_t g, const aa_block_config* c, int64_t n) {
+    return geo_of(n, *c).middle_end(g);
+}
+int64_t aa_anchor_covered_count(int64_t n, const aa_block_config* c) {
+    const aa::Geo G = geo_of(n, *c);
+    int64_t total = 0;
+    for (int64_t i = 0; i < n; ++i) total += G.covered_count_for_row(i);
+    return total;
+}
+int64_t aa_anchor_region(int64_t qb, const aa_block_config* c, int64_t n, int64_t* blocks,
+                         int64_t cap) {
+    const aa::Geo G = geo_of(n, *c);
+    if (qb < 0 || qb >= G.q_blocks()) {
+        g_err = "anchor_region: query block out of range";
+        return -1;
+    }
+    const int64_t last_row = ((qb + 1) * c->b_q < n ? (qb + 1) * c->b_q : n) - 1;
+    const int64_t diag = last_row / c->b_kv;
+    int64_t cnt = 0;
+    if (cnt < cap) blocks[cnt] = 0;
+    ++cnt;
+    for (int64_t b = G.window_start_block(qb / c->step); b <= diag && b < G.kv_blocks(); ++b) {
+        if (cnt < cap) blocks[cnt] = b;
+        ++cnt;
+    }
+    return cnt;
+}
+int64_t aa_stripe_offset(int64_t g, const aa_block_config* c, int64_t n) {
+    return geo_of(n, *c).stripe_offset(g);
+}
+
+aa_status aa_make_plan(const aa_problem* p, aa_plan* plan) {
+    if (!p || !plan) return fail(AA_ERR_INVALID_ARGUMENT, "aa_make_plan: null argument");
+    if (aa_status s = aa_config_validate(&p->cfg)) return s;
+    if (p->n < 1 || p->d < 1)
+        return fail(AA_ERR_INVALID_ARGUMENT, "HeadWorkload: n and d must be >= 1");
+    if (p->n > (int64_t(1) << 31) - 1)
+        return fail(AA_ERR_UNSUPPORTED, "n must fit 32-bit key indices (StripeIndex is uint32)");
+    if (p->hq < 1 || p->hkv < 1 || p->hq % p->hkv != 0)
+        return fail(AA_ERR_INVALID_ARGUMENT, "heads: hq must be a positive multiple of hkv");
+    if (p->dtype == AA_BF16) {
+        if (p->cfg.b_q != 128 || p->cfg.b_kv != 128 || p->d != 128)
+            return fail(AA_ERR_UNSUPPORTED,
+                        "bf16 tcgen05 path requires b_q == b_kv == 128 and d == 128");
+        const int64_t qrs = p->q_row_stride ? p->q_row_stride : p->d;
+        const int64_t krs = p->kv_row_stride ? p->kv_row_stride : p->d;
+        if ((qrs * 2) % 16 || (krs * 2) % 16)
+            return fail(AA_ERR_UNSUPPORTED, "bf16 path: row strides must be 16-byte multiples");
+    } else if (p->dtype != AA_F32) {
+        return fail(AA_ERR_UNSUPPORTED, "dtype must be AA_F32 (exact) or AA_BF16 (fast)");
+    }
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    plan->q_blocks = G.q_blocks();
+    plan->groups = G.groups();
+    plan->state_dtype = p->dtype == AA_BF16 ? AA_F32 : AA_F64;
+    plan->stripe_capacity = G.stripe_offset(G.groups());
+    plan->covered_positions = aa_anchor_covered_count(p->n, &p->cfg);
+    plan->workspace_bytes = 0;
+    plan->workspace_bytes = carve(*p, *plan, nullptr).total;
+    return AA_OK;
+}
+
+aa_status aa_stream_sync(aa_stream_t stream) {
+    AA_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    return AA_OK;
+}
+
+aa_status aa_device_count(int* count) {
+    *count = 0;
+    const cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return AA_OK;
+}
+
+aa_status aa_device_alloc(size_t bytes, void** ptr) {
+    if (aa_status s = require_device()) return s;
+    AA_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+    return AA_OK;
+}
+
+aa_status aa_device_free(void* ptr) {
+    if (ptr) AA_CUDA(cudaFree(ptr));
+    return AA_OK;
+}
+
+aa_status aa_copy_to_device(void* dst, const void* src, size_t bytes) {
+    if (bytes) AA_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return AA_OK;
+}
+
+aa_status aa_copy_to_host(void* dst, const void* src, size_t bytes) {
+    if (bytes) AA_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return AA_OK;
+}
+
+// ------------------------------------------------------------------ stages
+
+aa_status aa_compute_anchor(const aa_problem* p, const void* q, const void* k, const void* v,
+                            void* m, void* l, void* acc, float* qsum, double* msum,
+                            aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_anchor_exact(exact_args(*p), static_cast<const float*>(q),
+                                        static_cast<const float*>(k), static_cast<const float*>(v),
+                                        static_cast<double*>(m), static_cast<double*>(l),
+                                        static_cast<double*>(acc), st));
+    } else {
+        AA_CUDA(aa::fast_anchor(fast_args(*p), q, k, v, static_cast<float*>(m),
+                                static_cast<float*>(l), static_cast<float*>(acc), qsum, msum, st));
+    }
+    return AA_OK;
+}
+
+aa_status aa_pool(const aa_problem* p, const void* q, const void* m, const float* qsum,
+                  const double* msum, double* anchor, float* qbar, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_pool_exact(exact_args(*p), static_cast<const float*>(q),
+                                      static_cast<const double*>(m), anchor, qbar, st));
+    } else {
+        AA_CUDA(aa::fast_pool(fast_args(*p), q, static_cast<const float*>(m), qsum, msum, anchor,
+                              qbar, st));
+    }
+    return AA_OK;
+}
+
+static aa_status identify_impl(const aa_problem* p, const aa_plan& plan, const void* k,
+                               const float* qbar, const double* anchor, int zero_anchor,
+                               uint32_t* indices, int32_t* counts, int64_t* offsets_dev,
+                               uint32_t* bits, int64_t words_per_row, cudaStream_t st) {
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    const double* ref = zero_anchor ? nullptr : anchor;
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_identify_exact(exact_args(*p), static_cast<const float*>(k), qbar, ref,
+                                          bits, words_per_row, st));
+    } else {
+        AA_CUDA(aa::fast_identify(fast_args(*p), k, qbar, ref, bits, words_per_row, st));
+    }
+    AA_CUDA(aa::launch_offsets(G, offsets_dev, st));
+    AA_CUDA(aa::launch_compact(G, p->hq, bits, words_per_row, offsets_dev,
+                               plan.stripe_capacity > 0 ? plan.stripe_capacity : 1, indices,
+                               counts, st));
+    return AA_OK;
+}
+
+aa_status aa_identify(const aa_problem* p, const void* k, const float* qbar,
+                      const double* anchor, int zero_anchor, uint32_t* indices, int32_t* counts,
+                      void* workspace, size_t workspace_bytes, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (!zero_anchor && !anchor)
+        return fail(AA_ERR_INVALID_ARGUMENT, "aa_identify: anchor required unless zero_anchor");
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t wpr = (p->n + 31) / 32;
+    const size_t need = align256(static_cast<size_t>(plan.groups + 1) * 8) +
+                        static_cast<size_t>(p->hq * plan.groups * wpr) * 4;
+    Temp tmp(st);
+    char* base = static_cast<char*>(workspace);
+    if (!workspace || workspace_bytes < need) {
+        AA_CUDA(tmp.alloc(need));
+        base = static_cast<char*>(tmp.p);
+    }
+    int64_t* offs = reinterpret_cast<int64_t*>(base);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(base + align256(static_cast<size_t>(plan.groups + 1) * 8));
+    return identify_impl(p, plan, k, qbar, anchor, zero_anchor, indices, counts, offs, bits, wpr,
+                         st);
+}
+
+aa_status aa_sparse_attention(const aa_problem* p, const void* q, const void* k, const void* v,
+                              const void* m, const void* l, const void* acc,
+                              const uint32_t* indices, const int32_t* counts,
+                              const int64_t* offsets, int64_t fold_chunk, void* out,
+                              aa_dtype out_dtype, int64_t* computed, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (fold_chunk < 1)
+        return fail(AA_ERR_INVALID_ARGUMENT, "sparse_attention: index_chunk must be >= 1");
+    if (out_dtype != AA_F32 && out_dtype != AA_BF16)
+        return fail(AA_ERR_INVALID_ARGUMENT, "out_dtype must be AA_F32 or AA_BF16");
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    const int64_t cap = plan.stripe_capacity > 0 ? plan.stripe_capacity : 1;
+    Temp tmp(st);
+    AA_CUDA(tmp.alloc(align256(static_cast<size_t>(plan.groups + 1) * 8) +
+                      static_cast<size_t>(p->hq) * 8));
+    int64_t* offs = static_cast<int64_t*>(tmp.p);
+    unsigned long long* taken = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(tmp.p) + align256(static_cast<size_t>(plan.groups + 1) * 8));
+    // CSR tables index [h * groups + g] directly; the capacity layout adds h * cap.
+    int64_t row_cap = cap;
+    if (offsets) {
+        row_cap = 0;
+    } else {
+        AA_CUDA(aa::launch_offsets(G, offs, st));
+    }
+    const int64_t* offs_used = offsets ? offsets : offs;
+    if (p->dtype == AA_F32) {
+        AA_CUDA(cudaMemsetAsync(taken, 0, static_cast<size_t>(p->hq) * 8, st));
+        AA_CUDA(aa::launch_sparse_exact(
+            exact_args(*p), static_cast<const float*>(q), static_cast<const float*>(k),
+            static_cast<const float*>(v), static_cast<const double*>(m),
+            static_cast<const double*>(l), static_cast<const double*>(acc), indices, counts,
+            offs_used, row_cap, offsets != nullptr, fold_chunk, out, out_dtype, taken, st));
+        if (computed)
+            AA_CUDA(aa::launch_add_u64(p->hq, plan.covered_positions, taken, computed, st));
+    } else {
+        AA_CUDA(aa::fast_sparse(fast_args(*p), q, k, v, static_cast<const float*>(m),
+                                static_cast<const float*>(l), static_cast<const float*>(acc),
+                                indices, counts, offs_used, row_cap, offsets != nullptr, out,
+                                out_dtype, nullptr, st));
+        if (computed)
+            AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions, counts, computed, st));
+    }
+    return AA_OK;
+}
+
+aa_status aa_finalize_anchor(const aa_problem* p, const void* l, const void* acc, void* out,
+                             aa_dtype out_dtype, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_finalize_exact(exact_args(*p), static_cast<const double*>(l),
+                                          static_cast<const double*>(acc), out, out_dtype, st));
+    } else {
+        AA_CUDA(aa::fast_finalize(fast_args(*p), static_cast<const float*>(l),
+                                  static_cast<const float*>(acc), out, out_dtype, st));
+    }
+    return AA_OK;
+}
+
+aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k, const void* v,
+                              int zero_anchor, void* out, aa_dtype out_dtype, int64_t* computed,
+                              void* workspace, size_t workspace_bytes, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (out_dtype != AA_F32 && out_dtype != AA_BF16)
+        return fail(AA_ERR_INVALID_ARGUMENT, "out_dtype must be AA_F32 or AA_BF16");
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Temp tmp(st);
+    if (!workspace || workspace_bytes < plan.workspace_bytes) {
+        if (workspace)
+            return fail(AA_ERR_INVALID_ARGUMENT, "aa_anchor_attention: workspace too small");
+        AA_CUDA(tmp.alloc(plan.workspace_bytes));
+        workspace = tmp.p;
+    }
+    const Layout L = carve(*p, plan, workspace);
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    const int64_t cap = plan.stripe_capacity > 0 ? plan.stripe_capacity : 1;
+    if (p->dtype == AA_F32) {
+        const aa::ExactArgs a = exact_args(*p);
+        AA_CUDA(aa::launch_anchor_exact(a, static_cast<const float*>(q),
+                                        static_cast<const float*>(k), static_cast<const float*>(v),
+                                        static_cast<double*>(L.m), static_cast<double*>(L.l),
+                                        static_cast<double*>(L.acc), st));
+        AA_CUDA(aa::launch_pool_exact(a, static_cast<const float*>(q),
+                                      static_cast<const double*>(L.m),
+                                      static_cast<double*>(L.anchor), static_cast<float*>(L.qbar),
+                                      st));
+        if (aa_status s = identify_impl(p, plan, k, static_cast<float*>(L.qbar),
+                                        static_cast<double*>(L.anchor), zero_anchor,
+                                        static_cast<uint32_t*>(L.indices),
+                                        static_cast<int32_t*>(L.counts),
+                                        static_cast<int64_t*>(L.offsets),
+                                        static_cast<uint32_t*>(L.bits), L.words_per_row, st))
+            return s;
+        AA_CUDA(cudaMemsetAsync(L.taken, 0, static_cast<size_t>(p->hq) * 8, st));
+        AA_CUDA(aa::launch_sparse_exact(
+            a, static_cast<const float*>(q), static_cast<const float*>(k),
+            static_cast<const float*>(v), static_cast<double*>(L.m), static_cast<double*>(L.l),
+            static_cast<double*>(L.acc), static_cast<uint32_t*>(L.indices),
+            static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap, false, 64,
+            out, out_dtype, static_cast<unsigned long long*>(L.taken), st));
+        if (computed)
+            AA_CUDA(aa::launch_add_u64(p->hq, plan.covered_positions,
+                                       static_cast<unsigned long long*>(L.taken), computed, st));
+        return AA_OK;
+    }
+    const aa::FastArgs f = fast_args(*p);
+    AA_CUDA(aa::fast_anchor(f, q, k, v, static_cast<float*>(L.m), static_cast<float*>(L.l),
+                            static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
+                            static_cast<double*>(L.msum), st));
+    AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
+                          static_cast<double*>(L.msum), static_cast<double*>(L.anchor),
+                          static_cast<float*>(L.qbar), st));
+    if (aa_status s = identify_impl(p, plan, k, static_cast<float*>(L.qbar),
+                                    static_cast<double*>(L.anchor), zero_anchor,
+                                    static_cast<uint32_t*>(L.indices),
+                                    static_cast<int32_t*>(L.counts),
+                                    static_cast<int64_t*>(L.offsets),
+                                    static_cast<uint32_t*>(L.bits), L.words_per_row, st))
+        return s;
+    AA_CUDA(aa::fast_sparse(f, q, k, v, static_cast<float*>(L.m), static_cast<float*>(L.l),
+                            static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
+                            static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
+                            false, out, out_dtype, L.v16, st));
+    if (computed)
+        AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions,
+                                    static_cast<int32_t*>(L.counts), computed, st));
+    return AA_OK;
+}
+
+aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const void* k,
+                                   const void* v, int zero_anchor, void* out, aa_dtype out_dtype,
+                                   int64_t* computed) {
+    static std::mutex mu;
+    static void* dbuf = nullptr;
+    static size_t dbytes = 0;
+    static cudaStream_t st = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (p->q_row_stride || p->q_head_stride || p->kv_row_stride || p->kv_head_stride)
+        return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_host: packed layouts only");
+    if (aa_status s = require_device()) return s;
+    if (!st) AA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t es = p->dtype == AA_BF16 ? 2 : 4;
+    const size_t qb = static_cast<size_t>(p->hq * p->n * p->d) * es;
+    const size_t kvb = static_cast<size_t>(p->hkv * p->n * p->d) * es;
+    const size_t ob = static_cast<size_t>(p->hq * p->n * p->d) * (out_dtype == AA_BF16 ? 2 : 4);
+    const size_t cb = static_cast<size_t>(p->hq) * 8;
+    const size_t need = align256(qb) + 2 * align256(kvb) + align256(ob) + align256(cb) +
+                        plan.workspace_bytes;
+    if (need > dbytes) {
+        if (dbuf) AA_CUDA(cudaFree(dbuf));
+        dbuf = nullptr;
+        dbytes = 0;
+        AA_CUDA(cudaMalloc(&dbuf, need));
+        dbytes = need;
+    }
+    char* b = static_cast<char*>(dbuf);
+    void* dq = b;
+    void* dk = b + align256(qb);
+    void* dv = static_cast<char*>(dk) + align256(kvb);
+    void* dout = static_cast<char*>(dv) + align256(kvb);
+    int64_t* dc = reinterpret_cast<int64_t*>(static_cast<char*>(dout) + align256(ob));
+    void* ws = reinterpret_cast<char*>(dc) + align256(cb);
+    AA_CUDA(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, st));
+    AA_CUDA(cudaMemcpyAsync(dk, k, kvb, cudaMemcpyHostToDevice, st));
+    AA_CUDA(cudaMemcpyAsync(dv, v, kvb, cudaMemcpyHostToDevice, st));
+    if (aa_status s = aa_anchor_attention(p, dq, dk, dv, zero_anchor, dout, out_dtype, dc, ws,
+                                          plan.workspace_bytes, reinterpret_cast<aa_stream_t>(st)))
+        return s;
+    AA_CUDA(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, st));
+    if (computed) AA_CUDA(cudaMemcpyAsync(computed, dc, cb, cudaMemcpyDeviceToHost, st));
+    AA_CUDA(cudaStreamSynchronize(st));
+    return AA_OK;
+}
+
+aa_status aa_dense_attention(const aa_problem* p, const void* q, const void* k, const void* v,
+                             void* out, aa_dtype out_dtype, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_dense_exact(exact_args(*p), static_cast<const float*>(q),
+                                       static_cast<const float*>(k), static_cast<const float*>(v),
+                                       out, out_dtype, st));
+    } else {
+        AA_CUDA(aa::fast_dense(fast_args(*p), q, k, v, out, out_dtype, st));
+    }
+    return AA_OK;
+}
+
+aa_status aa_union_recall(const aa_problem* p, const void* q, const void* k,
+                          const uint32_t* indices, const int32_t* counts, double* recall,
+                          aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    const int64_t cap = plan.stripe_capacity > 0 ? plan.stripe_capacity : 1;
+    Temp tmp(st);
+    const size_t ob = align256(static_cast<size_t>(plan.groups + 1) * 8);
+    AA_CUDA(tmp.alloc(ob + static_cast<size_t>(p->hq * p->n) * 8));
+    int64_t* offs = static_cast<int64_t*>(tmp.p);
+    double* rows = reinterpret_cast<double*>(static_cast<char*>(tmp.p) + ob);
+    AA_CUDA(aa::launch_offsets(G, offs, st));
+    if (p->dtype == AA_F32) {
+        AA_CUDA(aa::launch_recall_exact(exact_args(*p), static_cast<const float*>(q),
+                                        static_cast<const float*>(k), indices, counts, offs, cap,
+                                        rows, recall, st));
+    } else {
+        AA_CUDA(aa::fast_recall(fast_args(*p), q, k, indices, counts, offs, cap, rows, recall,
+                                st));
+    }
+    return AA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// Fast path (aa_problem.dtype == AA_BF16): tcgen05 / TMEM / TMA kernels for
+// sm_100a with b_q == b_kv == 128 and d == 128.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace aa {
+
+struct FastArgs {
+    Geo geo;
+    int64_t hq, hkv, rep;
+    int64_t q_rs, q_hs, kv_rs, kv_hs;  // element strides (bf16 elements)
+    double theta;
+};
+
+// K1 — Alg. 1 anchor pass (tile list {0} ∪ [wsb(g), qb]); writes f32 m, l,
+// acc and the per-q-block partial sums qsum [hq, T_m, d] / msum [hq, T_m].
+cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v, float* m,
+                        float* l, float* acc, float* qsum, double* msum, cudaStream_t s);
+// Per-group pooled query (f32) and anchor (f64) from K1 partials (or from
+// q / m when the partials are NULL).
+cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const float* qsum,
+                      const double* msum, double* anchor, float* qbar, cudaStream_t s);
+// K2 — Alg. 2 scoring + threshold, one selection bit per candidate.
+cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
+                          const double* anchor, uint32_t* bits, int64_t words_per_row,
+                          cudaStream_t s);
+// K3 — Alg. 3 gathered-stripe fold resumed from (m, l, acc).  v16 is an
+// optional scratch of hkv*n*d fp16 for the converted V (NULL: allocate).
+cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v,
+                        const float* m, const float* l, const float* acc,
+                        const uint32_t* indices, const int32_t* counts, const int64_t* offsets,
+                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, void* v16,
+                        cudaStream_t s);
+cudaError_t fast_finalize(const FastArgs& f, const float* l, const float* acc, void* out,
+                          aa_dtype out_dtype, cudaStream_t s);
+// D — dense causal FlashAttention-style tcgen05 kernel (the speed baseline).
+cudaError_t fast_dense(const FastArgs& f, const void* q, const void* k, const void* v, void* out,
+                       aa_dtype out_dtype, cudaStream_t s);
+// Recall of the union mask from one dense pass.
+cudaError_t fast_recall(const FastArgs& f, const void* q, const void* k, const uint32_t* indices,
+                        const int32_t* counts, const int64_t* offsets, int64_t cap,
+                        double* row_captured, double* recall, cudaStream_t s);
+
+}  // namespace aa

@@ -1,0 +1,153 @@
+// anchorattn.hpp — the reference's C++ operator API (namespace anchorattn),
+// re-implemented over the B200 C ABI (include/anchorattn_capi.h).
+//
+// Same type names, member names, function signatures and exception types as
+// R/include/anchorattn/{matrix,anchor_pass,stripe_identify,sparse_exec,
+// selection_mask,oracle}.hpp (R/ = /root/reference/proj/), so call sites of
+// the reference compile unchanged.  Every value-producing call runs on the
+// GPU; there is no CPU fallback (std::runtime_error without a device).
+//
+// Precision: the reference takes f32 matrices and computes in f64.  The
+// default Precision::Exact runs the ABI's exact path (f64 GPU kernels, results
+// equal to the reference up to f64 round-off).  Precision::Bf16 (or
+// ANCHORATTN_PRECISION=bf16) rounds Q/K/V to bf16 and runs the tcgen05 path
+// when b_q == b_kv == 128 and d == 128 (the paper's kernels are FP16,
+// R/../PAPER.md Alg. 1 "REQUIRE FP16"); other shapes stay on the exact path.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <vector>
+
+namespace anchorattn {
+
+// ---- matrix.hpp ----------------------------------------------------------
+struct Matrix {
+    std::size_t rows = 0;
+    std::size_t cols = 0;
+    std::vector<float> data;
+
+    Matrix() = default;
+    Matrix(std::size_t r, std::size_t c, float fill = 0.0f) : rows(r), cols(c), data(r * c, fill) {}
+
+    float& at(std::size_t i, std::size_t j) { return data[i * cols + j]; }
+    float at(std::size_t i, std::size_t j) const { return data[i * cols + j]; }
+    std::span<const float> row(std::size_t i) const { return {data.data() + i * cols, cols}; }
+    std::span<float> row(std::size_t i) { return {data.data() + i * cols, cols}; }
+    bool same_shape(const Matrix& o) const { return rows == o.rows && cols == o.cols; }
+    bool all_finite() const;
+};
+
+struct HeadWorkload {
+    Matrix q, k, v;
+    std::size_t n = 0;
+    std::size_t d = 0;
+    static HeadWorkload create(Matrix q, Matrix k, Matrix v);
+};
+
+struct BlockConfig {
+    std::size_t b_q = 128;
+    std::size_t b_kv = 128;
+    std::size_t step = 1;  // C++ default of the reference (matrix.hpp:56)
+    double theta = 12.0;
+    void validate() const;
+};
+
+Matrix avgpool_rows(const Matrix& m, std::size_t block);
+std::vector<double> avgpool_vector(std::span<const double> v, std::size_t block);
+
+// ---- selection_mask.hpp --------------------------------------------------
+struct SelectionMask {
+    std::size_t n = 0;
+    std::vector<std::vector<std::uint32_t>> rows;
+
+    SelectionMask() = default;
+    explicit SelectionMask(std::size_t n_) : n(n_), rows(n_) {}
+    static SelectionMask full_causal(std::size_t n);
+    static SelectionMask empty(std::size_t n) { return SelectionMask(n); }
+    std::size_t total_selected() const;
+    std::size_t causal_positions() const { return n * (n + 1) / 2; }
+    bool contains(std::size_t i, std::uint32_t j) const;
+    void normalize();
+    bool valid() const;
+};
+
+// ---- oracle.hpp (output type) --------------------------------------------
+struct AttentionOutput {
+    Matrix o;
+};
+
+// ---- anchor_pass.hpp -----------------------------------------------------
+struct AnchorState {
+    std::size_t n = 0;
+    std::size_t d = 0;
+    BlockConfig cfg;
+    std::vector<double> m;
+    std::vector<double> l;
+    std::vector<double> acc;
+};
+
+std::vector<std::size_t> anchor_region(std::size_t q_block, const BlockConfig& cfg,
+                                       std::size_t n);
+std::size_t window_start_token(std::size_t group, const BlockConfig& cfg, std::size_t n);
+AnchorState compute_anchor(const HeadWorkload& w, const BlockConfig& cfg);
+SelectionMask anchor_mask(std::size_t n, const BlockConfig& cfg);
+std::size_t anchor_covered_count(std::size_t n, const BlockConfig& cfg);
+AttentionOutput finalize_anchor(const AnchorState& state);
+
+// ---- stripe_identify.hpp -------------------------------------------------
+struct StripeIndex {
+    std::size_t n = 0;
+    BlockConfig cfg;
+    std::vector<std::vector<std::uint32_t>> groups;
+
+    std::size_t group_count() const { return groups.size(); }
+    std::size_t f_c(std::size_t g) const { return groups[g].size(); }
+    std::size_t total_selected() const;
+    bool empty() const;
+};
+
+std::size_t group_count(std::size_t n, const BlockConfig& cfg);
+std::size_t middle_end_token(std::size_t group, const BlockConfig& cfg, std::size_t n);
+std::vector<double> pooled_anchor(const AnchorState& state, const BlockConfig& cfg);
+StripeIndex identify_stripes(const HeadWorkload& w, const AnchorState& state,
+                             const BlockConfig& cfg);
+StripeIndex identify_stripes_zero_anchor(const HeadWorkload& w, const BlockConfig& cfg);
+
+// ---- sparse_exec.hpp -----------------------------------------------------
+struct RunStats {
+    std::size_t computed_positions = 0;
+    std::size_t causal_positions = 0;
+    double sparsity = 0.0;
+    double recall = 0.0;
+};
+
+struct SparseResult {
+    AttentionOutput out;
+    RunStats stats;
+};
+
+struct FoldPlan {
+    std::size_t index_chunk = 64;
+    std::uint64_t shuffle_seed = 0;
+};
+
+SparseResult sparse_attention(const HeadWorkload& w, const AnchorState& state,
+                              const StripeIndex& idx, const BlockConfig& cfg,
+                              const FoldPlan& plan = {});
+SparseResult anchor_attention(const HeadWorkload& w, const BlockConfig& cfg,
+                              bool zero_anchor = false);
+SelectionMask union_mask(const StripeIndex& idx, const BlockConfig& cfg, std::size_t n);
+
+// ---- B200 additions --------------------------------------------------------
+enum class Precision { Exact, Bf16 };
+void set_precision(Precision p);
+Precision precision();
+
+/// Dense causal attention on the GPU (oracle.cpp:66-94 semantics).
+AttentionOutput dense_attention(const HeadWorkload& w);
+/// recall(union_mask(idx), dense_probs(q, k)) on the GPU (metrics.cpp:8-19).
+double union_recall(const HeadWorkload& w, const StripeIndex& idx, const BlockConfig& cfg);
+
+}  // namespace anchorattn
