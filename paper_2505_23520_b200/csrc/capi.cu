@@ -204,8 +204,11 @@ aa_status aa_make_plan(const aa_problem* p, aa_plan* plan) {
                         "bf16 tcgen05 path requires b_q == b_kv == 128 and d == 128");
         const int64_t qrs = p->q_row_stride ? p->q_row_stride : p->d;
         const int64_t krs = p->kv_row_stride ? p->kv_row_stride : p->d;
-        if ((qrs * 2) % 16 || (krs * 2) % 16)
-            return fail(AA_ERR_UNSUPPORTED, "bf16 path: row strides must be 16-byte multiples");
+        const int64_t khs = p->kv_head_stride ? p->kv_head_stride : p->n * krs;
+        if ((qrs * 2) % 16 || krs % p->d || khs % p->d)
+            return fail(AA_ERR_UNSUPPORTED,
+                        "bf16 path: q row stride must be a 16-byte multiple and k/v strides "
+                        "multiples of d (TMA gather rows)");
     } else if (p->dtype != AA_F32) {
         return fail(AA_ERR_UNSUPPORTED, "dtype must be AA_F32 (exact) or AA_BF16 (fast)");
     }
@@ -271,8 +274,12 @@ aa_status aa_compute_anchor(const aa_problem* p, const void* q, const void* k, c
                                         static_cast<double*>(m), static_cast<double*>(l),
                                         static_cast<double*>(acc), st));
     } else {
-        AA_CUDA(aa::fast_anchor(fast_args(*p), q, k, v, static_cast<float*>(m),
-                                static_cast<float*>(l), static_cast<float*>(acc), qsum, msum, st));
+        const aa::FastArgs f = fast_args(*p);
+        Temp v16(st);
+        AA_CUDA(v16.alloc(static_cast<size_t>(p->hkv * p->n * p->d) * 2));
+        AA_CUDA(aa::fast_convert_v(f, v, v16.p, st));
+        AA_CUDA(aa::fast_anchor(f, q, k, v16.p, static_cast<float*>(m), static_cast<float*>(l),
+                                static_cast<float*>(acc), qsum, msum, st));
     }
     return AA_OK;
 }
@@ -375,10 +382,14 @@ aa_status aa_sparse_attention(const aa_problem* p, const void* q, const void* k,
         if (computed)
             AA_CUDA(aa::launch_add_u64(p->hq, plan.covered_positions, taken, computed, st));
     } else {
-        AA_CUDA(aa::fast_sparse(fast_args(*p), q, k, v, static_cast<const float*>(m),
+        const aa::FastArgs f = fast_args(*p);
+        Temp v16(st);
+        AA_CUDA(v16.alloc(static_cast<size_t>(p->hkv * p->n * p->d) * 2));
+        AA_CUDA(aa::fast_convert_v(f, v, v16.p, st));
+        AA_CUDA(aa::fast_sparse(f, q, k, v16.p, static_cast<const float*>(m),
                                 static_cast<const float*>(l), static_cast<const float*>(acc),
                                 indices, counts, offs_used, row_cap, offsets != nullptr, out,
-                                out_dtype, nullptr, st));
+                                out_dtype, st));
         if (computed)
             AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions, counts, computed, st));
     }
@@ -450,7 +461,8 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
         return AA_OK;
     }
     const aa::FastArgs f = fast_args(*p);
-    AA_CUDA(aa::fast_anchor(f, q, k, v, static_cast<float*>(L.m), static_cast<float*>(L.l),
+    AA_CUDA(aa::fast_convert_v(f, v, L.v16, st));
+    AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
                             static_cast<double*>(L.msum), st));
     AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
@@ -463,10 +475,10 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
                                     static_cast<int64_t*>(L.offsets),
                                     static_cast<uint32_t*>(L.bits), L.words_per_row, st))
         return s;
-    AA_CUDA(aa::fast_sparse(f, q, k, v, static_cast<float*>(L.m), static_cast<float*>(L.l),
+    AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
                             static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
-                            false, out, out_dtype, L.v16, st));
+                            false, out, out_dtype, st));
     if (computed)
         AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions,
                                     static_cast<int32_t*>(L.counts), computed, st));
@@ -531,7 +543,11 @@ aa_status aa_dense_attention(const aa_problem* p, const void* q, const void* k, 
                                        static_cast<const float*>(k), static_cast<const float*>(v),
                                        out, out_dtype, st));
     } else {
-        AA_CUDA(aa::fast_dense(fast_args(*p), q, k, v, out, out_dtype, st));
+        const aa::FastArgs f = fast_args(*p);
+        Temp v16(st);
+        AA_CUDA(v16.alloc(static_cast<size_t>(p->hkv * p->n * p->d) * 2));
+        AA_CUDA(aa::fast_convert_v(f, v, v16.p, st));
+        AA_CUDA(aa::fast_dense(f, q, k, v16.p, out, out_dtype, st));
     }
     return AA_OK;
 }

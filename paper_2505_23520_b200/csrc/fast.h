@@ -17,9 +17,11 @@ struct FastArgs {
     double theta;
 };
 
+// V (bf16, strided) -> packed f16 copy [hkv, n, d] consumed by the PV MMAs.
+cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s);
 // K1 — Alg. 1 anchor pass (tile list {0} ∪ [wsb(g), qb]); writes f32 m, l,
 // acc and the per-q-block partial sums qsum [hq, T_m, d] / msum [hq, T_m].
-cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v, float* m,
+cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v16, float* m,
                         float* l, float* acc, float* qsum, double* msum, cudaStream_t s);
 // Per-group pooled query (f32) and anchor (f64) from K1 partials (or from
 // q / m when the partials are NULL).
@@ -29,17 +31,15 @@ cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const fl
 cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
                           const double* anchor, uint32_t* bits, int64_t words_per_row,
                           cudaStream_t s);
-// K3 — Alg. 3 gathered-stripe fold resumed from (m, l, acc).  v16 is an
-// optional scratch of hkv*n*d fp16 for the converted V (NULL: allocate).
-cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v,
+// K3 — Alg. 3 gathered-stripe fold resumed from (m, l, acc).
+cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v16,
                         const float* m, const float* l, const float* acc,
                         const uint32_t* indices, const int32_t* counts, const int64_t* offsets,
-                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, void* v16,
-                        cudaStream_t s);
+                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, cudaStream_t s);
 cudaError_t fast_finalize(const FastArgs& f, const float* l, const float* acc, void* out,
                           aa_dtype out_dtype, cudaStream_t s);
 // D — dense causal FlashAttention-style tcgen05 kernel (the speed baseline).
-cudaError_t fast_dense(const FastArgs& f, const void* q, const void* k, const void* v, void* out,
+cudaError_t fast_dense(const FastArgs& f, const void* q, const void* k, const void* v16, void* out,
                        aa_dtype out_dtype, cudaStream_t s);
 // Recall of the union mask from one dense pass.
 cudaError_t fast_recall(const FastArgs& f, const void* q, const void* k, const uint32_t* indices,
