@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""AnchorAttention prefill benchmark (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): Llama-3.1-8B attention shape at 128k
+tokens — 32 query heads / 8 KV heads, d = 128, b_q = b_kv = 128, step = 16,
+theta = 12 (the paper's operating point) — synthetic bf16 sink/stripe heads
+(paper_2505_23520_b200.workloads), generated on the GPU.
+
+One "step" = one prefill attention layer through the fused C-ABI chain
+(V->f16, K1 anchor, pool, K2 identify + compaction, K3 sparse, stats) with
+inputs resident in HBM.  value = ms per layer (lower is better).  With
+--gpus N (torchrun) the layer's KV heads (and their query heads) are sharded
+over the ranks with no data-path collective; ms/layer is the max over ranks
+(strong scaling: the layer is fixed).
+
+Also reported: per-stage device times (CUDA events recorded by the library
+on its own stream), the dominant kernel's roofline, the dense tcgen05 kernel
+on the same layer, e2e through the host-buffer C ABI entry
+(aa_anchor_attention_host: H2D q/k/v + chain + D2H out), and the reference
+CPU path timed on a bounded sample on this box's host cores.
+
+``--impl reference`` times the reference CPU implementation itself
+(oracle/_ref, the unmodified reference sources) on the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "128k prefill attention ms/layer & % roofline; sparsity at recall vs CPU ref"
+UNIT = "ms/layer"
+D = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--theta", type=float, default=12.0)
+    ap.add_argument("--step-blocks", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=2505)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=32768, help="reference sample length")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- utils
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def layer_geometry(n, step):
+    """covered positions and stripe candidates per head (closed form)."""
+    from paper_2505_23520_b200 import capi
+
+    cfg = capi.BlockConfig(128, 128, step, 12.0)
+    c = cfg.c()
+    import ctypes as C
+
+    covered = capi.lib().aa_anchor_covered_count(n, C.byref(c))
+    G = capi.lib().aa_group_count(n, C.byref(c))
+    offs = capi.stripe_offsets(n, cfg)
+    rows = [min((g + 1) * step * 128, n) - g * step * 128 for g in range(G)]
+    cand = sum((offs[g + 1] - offs[g]) * rows[g] for g in range(G))
+    return covered, cand
+
+
+def reference_sample(n_sample, heads, theta, step, seed, threads=None):
+    """Run the reference (oracle/_ref) anchor_attention on `heads` heads of the
+    synthetic workload at n_sample through its own parallel_for.  Returns
+    (wall_s, computed per head, candidates per head, covered per head)."""
+    import numpy as np
+
+    from oracle.oracle import Cfg, Reference
+    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
+
+    ref = Reference()
+    q, k, v = gen_sink_workload(SinkWorkloadSpec(n=n_sample, hq=heads, hkv=heads, seed=seed))
+    qn, kn, vn = (x.float().numpy() for x in (q, k, v))
+    if threads:
+        os.environ["ANCHOR_ATTN_THREADS"] = str(threads)
+    t0 = time.perf_counter()
+    _, computed = ref.layer(qn, kn, vn, Cfg(128, 128, step, theta))
+    wall = time.perf_counter() - t0
+    covered, cand = layer_geometry(n_sample, step)
+    return wall, computed, cand, covered
+
+
+def cpu_estimate(args, n_sample, heads, threads):
+    """Reference CPU ms/layer for the full workload, extrapolated by work:
+    rate = computed positions / s on the sample; the full layer's computed
+    positions use the sample's measured stripe-selection fraction."""
+    wall, computed, cand_s, cov_s = reference_sample(n_sample, heads, args.theta,
+                                                     args.step_blocks, args.seed, threads)
+    sel_frac = float((computed - cov_s).sum()) / (heads * cand_s) if cand_s else 0.0
+    rate = float(computed.sum()) / wall
+    cov_L, cand_L = layer_geometry(args.n, args.step_blocks)
+    layer_positions = args.hq * (cov_L + sel_frac * cand_L)
+    ms = layer_positions / rate * 1e3
+    sample = (f"reference anchor_attention (oracle/_ref) on {heads} synthetic heads at "
+              f"n={n_sample} via its parallel_for ({threads} threads): {wall:.2f} s, "
+              f"{rate:.3e} positions/s; extrapolated to the {args.hq}-head n={args.n} layer by "
+              f"computed positions (selection fraction {sel_frac:.4f})")
+    return ms, sample, wall
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    # per-head reference seconds ~ 0.8 s at 4k, x ~2.2 per doubling (SURVEY probe)
+    n_sample = 4096
+    for cand in (8192, 16384, 32768):
+        if 0.8 * (2.2 ** ((cand // 4096).bit_length() - 1)) <= per_step_budget:
+            n_sample = cand
+    heads = threads
+    vals = []
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        ms, sample, _ = cpu_estimate(args, n_sample, heads, threads)
+        if i >= args.warmup:
+            vals.append(ms)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"Llama-3.1-8B attention 32Q/8KV d=128, n={args.n}, theta={args.theta}, "
+                               f"b=128, step={args.step_blocks}", "global_batch": 1,
+                   "seq_len": args.n, "parallelism": "host threads over heads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_23520_b200 import capi
+    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.hkv % world:
+        raise SystemExit(f"hkv={args.hkv} must be divisible by the rank count {world}")
+    rep = args.hq // args.hkv
+    kv_local = args.hkv // world
+    kv0 = rank * kv_local
+    dev = torch.device("cuda", local)
+
+    # this rank's KV heads and their query heads; each KV head is generated from
+    # its own seed so the data does not depend on the rank count
+    qs, ks, vs = [], [], []
+    for kvh in range(kv0, kv0 + kv_local):
+        q, k, v = gen_sink_workload(SinkWorkloadSpec(n=args.n, hq=rep, hkv=1,
+                                                     seed=args.seed + kvh), device=dev)
+        qs.append(q), ks.append(k), vs.append(v)
+    q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
+    del qs, ks, vs
+    cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
+    pipe = capi.Pipeline(q, k, v, cfg)
+    hq_local = q.shape[0]
+    out = torch.empty((hq_local, args.n, D), dtype=torch.float32, device=dev)
+    computed = torch.empty(hq_local, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        pipe(q, k, v, out=out, computed=computed)
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    for row in evs:
+        for e in row:
+            e.record(stream)  # materialise the CUDA events
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0.record(stream)
+    for s in range(args.steps):
+        capi.set_stage_events(evs[s])
+        pipe(q, k, v, out=out, computed=computed)
+    capi.set_stage_events(None)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_local = t0.elapsed_time(t1) / args.steps
+    stage_ms = [statistics.mean(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps))
+                for i in range(5)]
+
+    comp_local = int(computed.sum().item())
+    covered, cand = layer_geometry(args.n, args.step_blocks)
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([comp_local], device=dev, dtype=torch.int64)
+        dist.all_reduce(c)
+        comp_total = int(c.item())
+    else:
+        ms, comp_total = ms_local, comp_local
+    causal = args.n * (args.n + 1) // 2
+    sparsity = 1.0 - comp_total / (args.hq * causal)
+
+    # roofline of the dominant kernel (this rank's launches)
+    peaks = measured_peaks()
+    tensor_peak = peaks.get("bf16_tflops", 1590.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured burst (MEASURED_PEAKS.json)" if peaks else "fallback (B200_PROFILING.md)"
+    k1_flops = 4.0 * D * hq_local * covered
+    k3_flops = 4.0 * D * (comp_local - hq_local * covered)
+    kernels = {
+        "k1_anchor": {"ms": stage_ms[1], "flops": k1_flops,
+                      "tflops": k1_flops / (stage_ms[1] * 1e-3) / 1e12},
+        "k3_sparse": {"ms": stage_ms[3], "flops": k3_flops,
+                      "tflops": k3_flops / (stage_ms[3] * 1e-3) / 1e12},
+    }
+    # K2 algorithmic bytes: K over the widest middle region once
+    # per KV head + pooled q (f32) and anchor (f64) per (head, group)
+    import ctypes as C
+
+    c_cfg = cfg.c()
+    G = capi.lib().aa_group_count(args.n, C.byref(c_cfg))
+    max_mid = max(0, capi.lib().aa_middle_end_token(G - 1, C.byref(c_cfg), args.n) - 128)
+    k2_bytes = kv_local * max_mid * D * 2 + hq_local * G * (D * 4 + 8)
+    kernels["k2_identify"] = {"ms": stage_ms[2], "bytes": k2_bytes,
+                              "gbs": k2_bytes / (stage_ms[2] * 1e-3) / 1e9}
+    dom = max(("k1_anchor", "k3_sparse"), key=lambda kname: kernels[kname]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except ValueError:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": kernels[dom]["tflops"],
+                "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": kernels[dom]["tflops"] / tensor_peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "work": f"4*d*positions = {kernels[dom]['flops']:.4e} FLOP per launch"}
+
+    # dense tcgen05 FlashAttention-style kernel on the same layer (baseline)
+    dense_ms = None
+    if not args.no_dense:
+        dout = torch.empty((hq_local, args.n, D), dtype=torch.bfloat16, device=dev)
+        capi.dense_attention(q, k, v, out=dout)
+        torch.cuda.synchronize()
+        reps = 2
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            capi.dense_attention(q, k, v, out=dout)
+        b.record(stream)
+        torch.cuda.synchronize()
+        dl = a.elapsed_time(b) / reps
+        if world > 1:
+            t = torch.tensor([dl], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dl = float(t.item())
+        dense_ms = dl
+        del dout
+
+    # e2e through the host-buffer C ABI entry (pinned host tensors)
+    e2e = None
+    if not args.no_e2e:
+        hq_h = q.cpu().pin_memory()
+        hk = k.cpu().pin_memory()
+        hv = v.cpu().pin_memory()
+        del pipe
+        torch.cuda.empty_cache()
+        capi.anchor_attention_host(hq_h, hk, hv, cfg)  # warm the cached device buffers
+        reps = max(2, min(args.steps, 5))
+        barrier()
+        tt = time.perf_counter()
+        for _ in range(reps):
+            o_h, c_h = capi.anchor_attention_host(hq_h, hk, hv, cfg)
+        e2e_ms = (time.perf_counter() - tt) * 1e3 / reps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = (hq_h.numel() + hk.numel() + hv.numel()) * 2
+        d2h = o_h.numel() * 4 + c_h.numel() * 8
+        if world > 1:
+            t = torch.tensor([h2d, d2h], device=dev, dtype=torch.int64)
+            dist.all_reduce(t)
+            h2d, d2h = int(t[0]), int(t[1])
+        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "path": "aa_anchor_attention_host (pinned host q/k/v -> device chain -> host out f32)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            ms_cpu, sample, _ = cpu_estimate(args, args.cpu_n, threads, threads)
+            cpu = {"value": ms_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": sample}
+        except Exception as exc:  # noqa: BLE001 - reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"Llama-3.1-8B attention 32Q/8KV d=128, n={args.n}, "
+                                   f"theta={args.theta}, b=128, step={args.step_blocks} "
+                                   "(BASELINE configs[2])",
+                       "global_batch": 1, "seq_len": args.n,
+                       "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (q/k/v 1.6 GB per layer), no flush"},
+            "sparsity": sparsity, "computed_positions": comp_total,
+            "stage_ms": dict(zip(capi.STAGES, stage_ms)),
+            "kernels": kernels,
+            "dense_ms_per_layer": dense_ms,
+            "speedup_vs_dense": (dense_ms / ms) if dense_ms else None,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 8 * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

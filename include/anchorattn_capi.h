@@ -180,6 +180,12 @@ aa_status aa_union_recall(const aa_problem* p, const void* q, const void* k,
                           const uint32_t* indices, const int32_t* counts, double* recall,
                           aa_stream_t stream);
 
+/* Stage timing for profilers/benchmarks: while set, the fast path of
+ * aa_anchor_attention records events[i] (cudaEvent_t) on its stream at the
+ * stage boundaries 0 start | 1 V->f16 | 2 K1 anchor | 3 pool + K2 identify +
+ * compaction | 4 K3 sparse | 5 stats.  Per calling thread; NULL disables. */
+aa_status aa_set_stage_events(void* const* events, int count);
+
 /* Plumbing for host callers that do not link the CUDA runtime themselves. */
 aa_status aa_stream_sync(aa_stream_t stream);
 aa_status aa_device_alloc(size_t bytes, void** ptr);

@@ -81,6 +81,7 @@ def lib():
             "aa_dense_attention": [P, p, p, p, p, C.c_int, p],
             "aa_union_recall": [P, p, p, p, p, p, p],
             "aa_stream_sync": [p],
+            "aa_set_stage_events": [C.POINTER(C.c_void_p), C.c_int],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -186,6 +187,20 @@ class Pipeline:
                                          _ptr(computed), _ptr(self.workspace),
                                          self.plan.workspace_bytes, _stream()))
         return out, computed
+
+
+STAGES = ("v_to_f16", "k1_anchor", "pool_k2_identify", "k3_sparse", "stats")
+
+
+def set_stage_events(events):
+    """Record ``events`` (6 torch.cuda.Event, or None) at the fused chain's
+    stage boundaries on the next calls from this thread (aa_set_stage_events)."""
+    if events is None:
+        _check(lib().aa_set_stage_events(None, 0))
+        return
+    arr = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
+    set_stage_events._keep = arr  # keep alive while registered
+    _check(lib().aa_set_stage_events(arr, len(events)))
 
 
 def anchor_attention(q, k, v, cfg=BlockConfig(), zero_anchor=False, out_dtype=torch.float32):

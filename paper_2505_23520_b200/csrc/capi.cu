@@ -19,6 +19,13 @@
 namespace {
 
 thread_local std::string g_err;
+// Optional per-stage timing events (aa_set_stage_events).
+thread_local void* const* g_events = nullptr;
+thread_local int g_nevents = 0;
+
+void mark(int i, cudaStream_t st) {
+    if (i < g_nevents && g_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(g_events[i]), st);
+}
 
 aa_status fail(aa_status s, const std::string& msg) {
     g_err = msg;
@@ -461,10 +468,13 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
         return AA_OK;
     }
     const aa::FastArgs f = fast_args(*p);
+    mark(0, st);
     AA_CUDA(aa::fast_convert_v(f, v, L.v16, st));
+    mark(1, st);
     AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
                             static_cast<double*>(L.msum), st));
+    mark(2, st);
     AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
                           static_cast<double*>(L.msum), static_cast<double*>(L.anchor),
                           static_cast<float*>(L.qbar), st));
@@ -475,13 +485,22 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
                                     static_cast<int64_t*>(L.offsets),
                                     static_cast<uint32_t*>(L.bits), L.words_per_row, st))
         return s;
+    mark(3, st);
     AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
                             static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
                             false, out, out_dtype, st));
+    mark(4, st);
     if (computed)
         AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions,
                                     static_cast<int32_t*>(L.counts), computed, st));
+    mark(5, st);
+    return AA_OK;
+}
+
+aa_status aa_set_stage_events(void* const* events, int count) {
+    g_events = events;
+    g_nevents = events ? count : 0;
     return AA_OK;
 }
 
