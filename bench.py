@@ -271,6 +271,9 @@ def run_ours(args):
     stage_ms = [statistics.mean(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps))
                 for i in range(5)]
 
+    print(f"[bench] rank {rank}: {ms_local:.3f} ms/layer-shard, stages "
+          + ", ".join(f"{nm}={t:.3f}" for nm, t in zip(capi.STAGES, stage_ms)), file=sys.stderr,
+          flush=True)
     comp_local = int(computed.sum().item())
     covered, cand = layer_geometry(args.n, args.step_blocks)
     if world > 1:
@@ -347,31 +350,34 @@ def run_ours(args):
     # e2e through the host-buffer C ABI entry (pinned host tensors)
     e2e = None
     if not args.no_e2e:
-        hq_h = q.cpu().pin_memory()
-        hk = k.cpu().pin_memory()
-        hv = v.cpu().pin_memory()
-        del pipe
-        torch.cuda.empty_cache()
-        capi.anchor_attention_host(hq_h, hk, hv, cfg)  # warm the cached device buffers
-        reps = max(2, min(args.steps, 5))
-        barrier()
-        tt = time.perf_counter()
-        for _ in range(reps):
-            o_h, c_h = capi.anchor_attention_host(hq_h, hk, hv, cfg)
-        e2e_ms = (time.perf_counter() - tt) * 1e3 / reps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        h2d = (hq_h.numel() + hk.numel() + hv.numel()) * 2
-        d2h = o_h.numel() * 4 + c_h.numel() * 8
-        if world > 1:
-            t = torch.tensor([h2d, d2h], device=dev, dtype=torch.int64)
-            dist.all_reduce(t)
-            h2d, d2h = int(t[0]), int(t[1])
-        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
-               "path": "aa_anchor_attention_host (pinned host q/k/v -> device chain -> host out f32)"}
+        try:
+            hq_h = q.cpu().pin_memory()
+            hk = k.cpu().pin_memory()
+            hv = v.cpu().pin_memory()
+            del pipe
+            torch.cuda.empty_cache()
+            capi.anchor_attention_host(hq_h, hk, hv, cfg)  # warm the cached device buffers
+            reps = max(2, min(args.steps, 5))
+            barrier()
+            tt = time.perf_counter()
+            for _ in range(reps):
+                o_h, c_h = capi.anchor_attention_host(hq_h, hk, hv, cfg)
+            e2e_ms = (time.perf_counter() - tt) * 1e3 / reps
+            if world > 1:
+                t = torch.tensor([e2e_ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e2e_ms = float(t.item())
+            h2d = (hq_h.numel() + hk.numel() + hv.numel()) * 2
+            d2h = o_h.numel() * 4 + c_h.numel() * 8
+            if world > 1:
+                t = torch.tensor([h2d, d2h], device=dev, dtype=torch.int64)
+                dist.all_reduce(t)
+                h2d, d2h = int(t[0]), int(t[1])
+            e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h,
+                   "path": "aa_anchor_attention_host (pinned host q/k/v -> device chain -> host out f32)"}
+        except Exception as exc:  # noqa: BLE001 - reported in the line
+            e2e = {"value": None, "unit": UNIT, "error": str(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

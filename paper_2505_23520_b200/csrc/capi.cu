@@ -514,7 +514,9 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     std::lock_guard<std::mutex> lock(mu);
     aa_plan plan;
     if (aa_status s = aa_make_plan(p, &plan)) return s;
-    if (p->q_row_stride || p->q_head_stride || p->kv_row_stride || p->kv_head_stride)
+    const auto packed = [&](int64_t s, int64_t want) { return s == 0 || s == want; };
+    if (!packed(p->q_row_stride, p->d) || !packed(p->q_head_stride, p->n * p->d) ||
+        !packed(p->kv_row_stride, p->d) || !packed(p->kv_head_stride, p->n * p->d))
         return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_host: packed layouts only");
     if (aa_status s = require_device()) return s;
     if (!st) AA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
