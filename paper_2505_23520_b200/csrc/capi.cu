@@ -46,6 +46,9 @@ aa::Geo geo_of(int64_t n, const aa_block_config& c) { return aa::Geo{n, c.b_q, c
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Selection-bitmask row pitch in 32-bit words (multiple of 4: 16-byte stores).
+int64_t words_per_row(int64_t n) { return ((n + 31) / 32 + 3) / 4 * 4; }
+
 // Buffers of the fused chain, carved from one workspace.
 struct Carve {
     size_t off = 0;
@@ -72,7 +75,7 @@ Layout carve(const aa_problem& p, const aa_plan& plan, void* ws) {
     const size_t hq = static_cast<size_t>(p.hq), n = static_cast<size_t>(p.n),
                  d = static_cast<size_t>(p.d), G = static_cast<size_t>(plan.groups),
                  T = static_cast<size_t>(plan.q_blocks);
-    L.words_per_row = (p.n + 31) / 32;
+    L.words_per_row = words_per_row(p.n);
     L.m = c.take(hq * n * se);
     L.l = c.take(hq * n * se);
     L.acc = c.take(hq * n * d * se);
@@ -335,7 +338,7 @@ aa_status aa_identify(const aa_problem* p, const void* k, const float* qbar,
         return fail(AA_ERR_INVALID_ARGUMENT, "aa_identify: anchor required unless zero_anchor");
     if (aa_status s = require_device()) return s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int64_t wpr = (p->n + 31) / 32;
+    const int64_t wpr = words_per_row(p->n);
     const size_t need = align256(static_cast<size_t>(plan.groups + 1) * 8) +
                         static_cast<size_t>(p->hq * plan.groups * wpr) * 4;
     Temp tmp(st);

@@ -84,7 +84,6 @@ struct Smem {
         bar_o_done;
     uint32_t tmem_base;
     float red[4];
-    uint32_t gidx[kB];
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
@@ -151,55 +150,60 @@ __global__ void __launch_bounds__(kThreads, 2)
             tma_load_3d(S.q, &tmQ, &S.bar_q, 0, qb * kB, h);
             tma_load_3d(S.q + kAtomBytes, &tmQ, &S.bar_q, 64, qb * kB, h);
         }
-        for (int it = 0; it < ntiles; ++it) {
-            if (MODE == SPARSE) {
-                // stage this tile's 128 key indices (tail padded with the first)
-                const int base = it * kB;
-                for (int r = lane; r < kB; r += 32) {
-                    const int e = base + r;
-                    S.gidx[r] = list[e < count ? e : base];
+        if (MODE == SPARSE) {
+            // Every lane gathers 4 of the tile's 128 rows (gather4 x 2 column
+            // halves, for K and for V), so a tile is 4 TMA issues per lane
+            // instead of 128 from one thread.  The next tile's indices are
+            // fetched while this tile's loads are in flight.
+            auto fetch = [&](int t, int (&j)[4]) {
+                const int base = t * kB;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = base + lane * 4 + u;
+                    j[u] = static_cast<int>(list[e < count ? e : base]);
+                }
+            };
+            int j[4];
+            if (ntiles > 0) fetch(0, j);
+            const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
+            uint8_t* kdst = S.k + lane * 4 * 128;
+            uint8_t* vdst = S.v + lane * 4 * 128;
+            for (int it = 0; it < ntiles; ++it) {
+                int rk[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) rk[u] = kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
+                if (lane == 0) {
+                    if (it > 0) mbar_wait(&S.bar_k_empty, (it - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full, kTileBytes);
                 }
                 __syncwarp();
+                tma_gather4(kdst, &tmKg, &S.bar_k_full, 0, rk[0], rk[1], rk[2], rk[3]);
+                tma_gather4(kdst + kAtomBytes, &tmKg, &S.bar_k_full, 64, rk[0], rk[1], rk[2], rk[3]);
+                if (lane == 0) {
+                    if (it > 0) mbar_wait(&S.bar_v_empty, (it - 1) & 1);
+                    mbar_expect_tx(&S.bar_v_full, kTileBytes);
+                }
+                __syncwarp();
+                tma_gather4(vdst, &tmVg, &S.bar_v_full, 0, vh + j[0], vh + j[1], vh + j[2], vh + j[3]);
+                tma_gather4(vdst + kAtomBytes, &tmVg, &S.bar_v_full, 64, vh + j[0], vh + j[1],
+                            vh + j[2], vh + j[3]);
+                if (it + 1 < ntiles) fetch(it + 1, j);
             }
-            if (lane == 0) {
-                if (it > 0) mbar_wait(&S.bar_k_empty, (it - 1) & 1);
-                mbar_expect_tx(&S.bar_k_full, kTileBytes);
-                if (MODE == SPARSE) {
-                    for (int r = 0; r < kB; r += 4) {
-                        int rows[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            rows[u] = kvh * P.kv_head_rows + static_cast<int>(S.gidx[r + u]) * P.kv_row_rows;
-                        tma_gather4(S.k + r * 128, &tmKg, &S.bar_k_full, 0, rows[0], rows[1], rows[2], rows[3]);
-                        tma_gather4(S.k + kAtomBytes + r * 128, &tmKg, &S.bar_k_full, 64, rows[0],
-                                    rows[1], rows[2], rows[3]);
-                    }
-                } else {
+        } else {
+            for (int it = 0; it < ntiles; ++it) {
+                if (lane == 0) {
                     const int kt = kv_tile_of(MODE, it, wsb);
+                    if (it > 0) mbar_wait(&S.bar_k_empty, (it - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full, kTileBytes);
                     tma_load_3d(S.k, &tmK, &S.bar_k_full, 0, kt * kB, kvh);
                     tma_load_3d(S.k + kAtomBytes, &tmK, &S.bar_k_full, 64, kt * kB, kvh);
-                }
-                if (it > 0) mbar_wait(&S.bar_v_empty, (it - 1) & 1);
-                mbar_expect_tx(&S.bar_v_full, kTileBytes);
-                if (MODE == SPARSE) {
-                    for (int r = 0; r < kB; r += 4) {
-                        const int rows0 = static_cast<int>(S.gidx[r + 0]);
-                        const int rows1 = static_cast<int>(S.gidx[r + 1]);
-                        const int rows2 = static_cast<int>(S.gidx[r + 2]);
-                        const int rows3 = static_cast<int>(S.gidx[r + 3]);
-                        const int hb = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
-                        tma_gather4(S.v + r * 128, &tmVg, &S.bar_v_full, 0, hb + rows0, hb + rows1,
-                                    hb + rows2, hb + rows3);
-                        tma_gather4(S.v + kAtomBytes + r * 128, &tmVg, &S.bar_v_full, 64, hb + rows0,
-                                    hb + rows1, hb + rows2, hb + rows3);
-                    }
-                } else {
-                    const int kt = kv_tile_of(MODE, it, wsb);
+                    if (it > 0) mbar_wait(&S.bar_v_empty, (it - 1) & 1);
+                    mbar_expect_tx(&S.bar_v_full, kTileBytes);
                     tma_load_3d(S.v, &tmV, &S.bar_v_full, 0, kt * kB, kvh);
                     tma_load_3d(S.v + kAtomBytes, &tmV, &S.bar_v_full, 64, kt * kB, kvh);
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
@@ -445,74 +449,179 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ------------------------------------------------------------------------ K2
-// Alg. 2 (R/src/stripe_identify.cpp:31-46) for one KV head and one 128-key
-// tile: every (query head of the GQA group, group g whose middle region
-// reaches the tile) scores the tile against its pooled query in f32 and
-// emits one selection bit per key (ballot).  grid (key tiles, hkv), 256 thr.
-__global__ void __launch_bounds__(256)
-    k_identify_fast(Geo geo, int hq, int rep, int64_t kv_rs, int64_t kv_hs,
-                    const __nv_bfloat16* __restrict__ k, const float* __restrict__ qbar,
-                    const double* __restrict__ anchor, double theta, float inv_sqrt_d,
-                    uint32_t* __restrict__ bits, int64_t words_per_row) {
-    __shared__ float sq[8][kD];
+// Alg. 2 (R/src/stripe_identify.cpp:31-46) on the tensor cores.
+//
+// For one KV head, the pooled queries of its GQA query heads form the rows
+// r = g * rep + hh (group-major) of an A operand; 128 rows per CTA (one
+// M-tile).  q_bar is f32 in the reference; it enters the MMA as an exact-ish
+// split q_bar = hi + lo (two bf16 terms, residual ~2^-17 |q_bar|), so
+// S = hi K^T + lo K^T is the f32 score to ~1e-5 — far inside the +-1e-3
+// selection band — while K streams from HBM once per (head, M-tile).
+// Each TMEM lane holds one (head, group) row, so its thread assembles the
+// 32-bit selection words of 32 consecutive keys directly (no ballot).
+//
+// grid (chunks of key tiles, M-tiles, hkv); 192 threads: warp 0 TMA,
+// warp 1 MMA, warps 2-5 threshold + bit words.  K ring of 2 stages, 2 TMEM
+// accumulators.
+constexpr int kIdChunk = 16;  // key tiles per CTA
+
+struct IdSmem {
+    uint8_t a_hi[kTileBytes];
+    uint8_t a_lo[kTileBytes];
+    uint8_t k[2][kTileBytes];
+    uint64_t bar_a, bar_k_full[2], bar_k_empty[2], bar_s_full[2], bar_s_empty[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_identify_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmK,
+                  Geo geo, int rep, int rows_pad, const double* __restrict__ anchor, double theta,
+                  uint32_t* __restrict__ bits, int64_t words_per_row) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    IdSmem& S = *reinterpret_cast<IdSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kvh = blockIdx.z;
+    const int mt = blockIdx.y;
     const int groups = static_cast<int>(geo.groups());
+    // key tiles relevant to this M-tile: up to the widest middle region of its groups
+    const int g_last = min(groups - 1, ((mt + 1) * kB - 1) / rep);
+    const int64_t span = geo.middle_end(g_last) - geo.b_kv;
+    const int tiles_total = span > 0 ? static_cast<int>((span + kB - 1) / kB) : 0;
+    const int t0 = blockIdx.x * kIdChunk;
+    const int nt = max(0, min(kIdChunk, tiles_total - t0));
+    if (nt == 0) return;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar_a, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&S.bar_k_full[b], 1);
+            mbar_init(&S.bar_k_empty[b], 1);
+            mbar_init(&S.bar_s_full[b], 1);
+            mbar_init(&S.bar_s_empty[b], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(&S.tmem_base, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(&S.bar_a, 2 * kTileBytes);
+            const int arow = mt * kB;
+            tma_load_3d(S.a_hi, &tmA, &S.bar_a, 0, arow, 2 * kvh);
+            tma_load_3d(S.a_hi + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh);
+            tma_load_3d(S.a_lo, &tmA, &S.bar_a, 0, arow, 2 * kvh + 1);
+            tma_load_3d(S.a_lo + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh + 1);
+            for (int i = 0; i < nt; ++i) {
+                const int b = i & 1;
+                if (i >= 2) mbar_wait(&S.bar_k_empty[b], ((i >> 1) - 1) & 1);
+                mbar_expect_tx(&S.bar_k_full[b], kTileBytes);
+                const int key0 = static_cast<int>(geo.b_kv) + (t0 + i) * kB;
+                tma_load_3d(S.k[b], &tmK, &S.bar_k_full[b], 0, key0, kvh);
+                tma_load_3d(S.k[b] + kAtomBytes, &tmK, &S.bar_k_full[b], 64, key0, kvh);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t ah = smem_u32(S.a_hi), al = smem_u32(S.a_lo);
+            mbar_wait(&S.bar_a, 0);
+            for (int i = 0; i < nt; ++i) {
+                const int b = i & 1;
+                mbar_wait(&S.bar_k_full[b], (i >> 1) & 1);
+                if (i >= 2) mbar_wait(&S.bar_s_empty[b], ((i >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t kb = smem_u32(S.k[b]);
+                const uint32_t d_tmem = tmem + b * 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+                    mma_ss(d_tmem, sdesc_sw128(ah + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                           kIdescQK, kk > 0 ? 1u : 0u);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+                    mma_ss(d_tmem, sdesc_sw128(al + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                           kIdescQK, 1u);
+                }
+                mma_commit(&S.bar_s_full[b]);
+                mma_commit(&S.bar_k_empty[b]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int grow = mt * kB + r;
+        const int g = grow / rep, hh = kvh * rep + grow % rep;
+        const bool valid = grow < groups * rep;
+        int64_t mend = 0;
+        float thr = 0.f;
+        if (valid) {
+            mend = geo.middle_end(g);
+            const double ref = anchor ? anchor[static_cast<int64_t>(hh) * groups + g] : 0.0;
+            // keep iff ref - s*inv_sqrt_d <= theta  <=>  s >= (ref - theta) * sqrt(d)
+            thr = static_cast<float>((ref - theta) * sqrt(static_cast<double>(kD)));
+        }
+        uint32_t* rowbits = bits + (static_cast<int64_t>(hh) * groups + g) * words_per_row;
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        for (int i = 0; i < nt; ++i) {
+            const int b = i & 1;
+            mbar_wait(&S.bar_s_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            const int64_t key0 = geo.b_kv + static_cast<int64_t>(t0 + i) * kB;
+            uint32_t w[4];
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t v[32];
+                tmem_ld32(tmem + b * 128 + lane_off + ch * 32, v);
+                tmem_wait_ld();
+                uint32_t word = 0;
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    word |= (__uint_as_float(v[c]) >= thr ? 1u : 0u) << c;
+                const int64_t kfirst = key0 + ch * 32;
+                if (kfirst + 32 > mend) {
+                    const int64_t keep = mend - kfirst;
+                    word = keep <= 0 ? 0u : (keep >= 32 ? word : word & ((1u << keep) - 1u));
+                }
+                w[ch] = word;
+            }
+            tc_fence_before();
+            mbar_arrive(&S.bar_s_empty[b]);
+            if (valid && key0 < mend) {
+                const int64_t word0 = (key0 - geo.b_kv) >> 5;
+                *reinterpret_cast<uint4*>(rowbits + word0) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+// q_bar (f32 [hq, G, d]) -> A operand rows r = g*rep + hh of KV head kvh as a
+// two-term bf16 split: out[(2*kvh + 0), r, :] = hi, out[(2*kvh + 1), r, :] = lo.
+__global__ void k_split_qbar(int groups, int rep, int rows_pad, const float* __restrict__ qbar,
+                             __nv_bfloat16* __restrict__ out) {
     const int kvh = blockIdx.y;
-    const int64_t key0 = geo.b_kv + static_cast<int64_t>(blockIdx.x) * kB;
-    const int key = threadIdx.x & 127;
-    const int half = threadIdx.x >> 7;
-    const int64_t j = key0 + key;
-    // this thread's key row in registers (f32)
-    float kr[kD];
-    const bool in_range = j < geo.n;
-    const __nv_bfloat16* krow = k + kvh * kv_hs + (in_range ? j : 0) * kv_rs;
-#pragma unroll
-    for (int t = 0; t < kD; t += 8) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(krow + t);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float2 f = __bfloat1622float2(p2[u]);
-            kr[t + 2 * u] = f.x;
-            kr[t + 2 * u + 1] = f.y;
-        }
+    const int r = blockIdx.x;
+    const int t = threadIdx.x;
+    float x = 0.f;
+    if (r < groups * rep) {
+        const int g = r / rep, hh = kvh * rep + r % rep;
+        x = qbar[(static_cast<int64_t>(hh) * groups + g) * kD + t];
     }
-    // first group whose middle region contains key0: middle_end(g) > key0
-    int g_first = groups;
-    for (int gg = 0; gg < groups; ++gg)
-        if (geo.middle_end(gg) > key0) { g_first = gg; break; }
-    const int npairs = rep * (groups - g_first);
-    for (int base = 0; base < npairs; base += 8) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < 8 * kD; e += blockDim.x) {
-            const int pi = base + e / kD;
-            if (pi < npairs) {
-                const int hh = kvh * rep + pi % rep, gg = g_first + pi / rep;
-                sq[e / kD][e % kD] = qbar[(static_cast<int64_t>(hh) * groups + gg) * kD + e % kD];
-            }
-        }
-        __syncthreads();
-        for (int s = half; s < 8 && base + s < npairs; s += 2) {
-            const int pi = base + s;
-            const int hh = kvh * rep + pi % rep, gg = g_first + pi / rep;
-            const int64_t mend = geo.middle_end(gg);
-            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-#pragma unroll
-            for (int t = 0; t < kD; t += 4) {
-                acc0 = fmaf(sq[s][t], kr[t], acc0);
-                acc1 = fmaf(sq[s][t + 1], kr[t + 1], acc1);
-                acc2 = fmaf(sq[s][t + 2], kr[t + 2], acc2);
-                acc3 = fmaf(sq[s][t + 3], kr[t + 3], acc3);
-            }
-            const float sc = ((acc0 + acc1) + (acc2 + acc3)) * inv_sqrt_d;
-            const double ref = anchor ? anchor[static_cast<int64_t>(hh) * groups + gg] : 0.0;
-            const bool keep = j < mend && (ref - static_cast<double>(sc) <= theta);
-            const uint32_t w = __ballot_sync(0xffffffffu, keep);
-            if ((threadIdx.x & 31) == 0 && key0 + (key & ~31) < mend) {
-                const int64_t word = (key0 - geo.b_kv + key) >> 5;
-                bits[(static_cast<int64_t>(hh) * groups + gg) * words_per_row + word] = w;
-            }
-        }
-    }
+    const __nv_bfloat16 hi = __float2bfloat16(x);
+    const __nv_bfloat16 lo = __float2bfloat16(x - __bfloat162float(hi));
+    out[((2 * static_cast<int64_t>(kvh)) * rows_pad + r) * kD + t] = hi;
+    out[((2 * static_cast<int64_t>(kvh) + 1) * rows_pad + r) * kD + t] = lo;
 }
 
 // Pooled query / anchor per group from K1's per-query-block partials
@@ -706,11 +815,41 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     const int64_t span = max_end > f.geo.b_kv ? max_end - f.geo.b_kv : 0;
     const int64_t tiles = (span + kB - 1) / kB;
     if (tiles == 0) return cudaSuccess;
-    k_identify_fast<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(f.hkv)), 256, 0, s>>>(
-        f.geo, static_cast<int>(f.hq), static_cast<int>(f.rep), f.kv_rs, f.kv_hs,
-        static_cast<const __nv_bfloat16*>(k), qbar, anchor, f.theta,
-        1.0f / sqrtf(static_cast<float>(kD)), bits, words_per_row);
-    return cudaGetLastError();
+    if (words_per_row % 4) return cudaErrorInvalidValue;  // 16-byte word stores
+    const int rows = static_cast<int>(G * f.rep);
+    const int rows_pad = (rows + kB - 1) / kB * kB;
+    void* split = nullptr;
+    cudaError_t e;
+    const size_t split_bytes = static_cast<size_t>(2 * f.hkv) * rows_pad * kD * 2;
+    if ((e = cudaMallocAsync(&split, split_bytes, s))) return e;
+    k_split_qbar<<<dim3(static_cast<unsigned>(rows_pad), static_cast<unsigned>(f.hkv)), kD, 0, s>>>(
+        static_cast<int>(G), static_cast<int>(f.rep), rows_pad, qbar,
+        static_cast<__nv_bfloat16*>(split));
+    CUtensorMap ta, tk;
+    if ((e = make_map_3d(&ta, split, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rows_pad, 2 * f.hkv, kD,
+                         static_cast<int64_t>(rows_pad) * kD)) ||
+        (e = make_map_3d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f.geo.n, f.hkv, f.kv_rs,
+                         f.kv_hs))) {
+        cudaFreeAsync(split, s);
+        return e;
+    }
+    constexpr size_t smem = sizeof(IdSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        if ((e = cudaFuncSetAttribute(k_identify_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)))) {
+            cudaFreeAsync(split, s);
+            return e;
+        }
+        attr = true;
+    }
+    const unsigned chunks = static_cast<unsigned>((tiles + kIdChunk - 1) / kIdChunk);
+    k_identify_tc<<<dim3(chunks, static_cast<unsigned>(rows_pad / kB), static_cast<unsigned>(f.hkv)),
+                    kThreads, smem, s>>>(ta, tk, f.geo, static_cast<int>(f.rep), rows_pad, anchor,
+                                         f.theta, bits, words_per_row);
+    e = cudaGetLastError();
+    cudaFreeAsync(split, s);
+    return e;
 }
 
 cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v16,
