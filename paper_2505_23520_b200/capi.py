@@ -297,11 +297,14 @@ def union_recall(q, k, idx, counts, cfg=BlockConfig()):
 
 
 def anchor_attention_host(q, k, v, cfg=BlockConfig(), zero_anchor=False,
-                          out_dtype=torch.float32):
+                          out_dtype=torch.float32, out=None, computed=None):
     """The chain on HOST (pinned) tensors through aa_anchor_attention_host."""
     p = make_problem(q, k, cfg)
-    out = torch.empty(q.shape, dtype=out_dtype, pin_memory=q.is_pinned())
-    computed = torch.empty(q.shape[0], dtype=torch.int64)
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, pin_memory=q.is_pinned())
+    out_dtype = out.dtype
+    if computed is None:
+        computed = torch.empty(q.shape[0], dtype=torch.int64, pin_memory=q.is_pinned())
     _check(lib().aa_anchor_attention_host(C.byref(p), _ptr(q), _ptr(k), _ptr(v),
                                           int(zero_anchor), _ptr(out), _out_code(out_dtype),
                                           _ptr(computed)))
