@@ -1,0 +1,84 @@
+"""Multi-rank host logic of KV-head sharding (world_size 2, gloo, CPU) and the
+sharded layer on one GPU (every rank's shard run in turn equals the full run)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2505_23520_b200.sharding import (gather_heads, local_slices, max_over_ranks,
+                                            shard_heads)
+
+
+def test_shard_assignment_covers_heads_once():
+    for hq, hkv, world in [(32, 8, 1), (32, 8, 2), (32, 8, 4), (32, 8, 8), (28, 4, 2), (28, 4, 4)]:
+        seen_q, seen_kv = [], []
+        for r in range(world):
+            s = shard_heads(hq, hkv, r, world)
+            seen_q += list(range(s.q_begin, s.q_end))
+            seen_kv += list(range(s.kv_begin, s.kv_end))
+            for h in range(s.q_begin, s.q_end):  # GQA: query head reads a local KV head
+                assert s.kv_begin <= h // (hq // hkv) < s.kv_end
+        assert seen_q == list(range(hq)) and seen_kv == list(range(hkv))
+    with pytest.raises(ValueError):
+        shard_heads(28, 4, 0, 8)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q, k, v, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shard = shard_heads(q.shape[0], k.shape[0], rank, world)
+    ql, kl, vl = local_slices(q, k, v, shard)
+    rep = q.shape[0] // k.shape[0]
+    # stand-in per-head op with the same head->KV-head dependence as attention
+    out_local = ql * kl.repeat_interleave(rep, 0) + vl.repeat_interleave(rep, 0)
+    full = gather_heads(out_local)
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        ret["full"] = full
+        ret["max"] = t
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_gather_and_max():
+    world = 2
+    q = torch.randn(8, 16, 4)
+    k = torch.randn(2, 16, 4)
+    v = torch.randn(2, 16, 4)
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), q, k, v, ret), nprocs=world, join=True)
+    expect = q * k.repeat_interleave(4, 0) + v.repeat_interleave(4, 0)
+    assert torch.equal(ret["full"], expect)
+    assert ret["max"] == 2.0
+
+
+@pytest.mark.gpu
+def test_sharded_layer_equals_full_layer():
+    from paper_2505_23520_b200 import capi
+    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
+
+    q, k, v = gen_sink_workload(SinkWorkloadSpec(n=8192, hq=8, hkv=4, seed=17), device="cuda")
+    cfg = capi.BlockConfig()
+    full, comp = capi.anchor_attention(q, k, v, cfg)
+    for world in (2, 4):
+        parts, comps = [], []
+        for r in range(world):
+            s = shard_heads(8, 4, r, world)
+            o, c = capi.anchor_attention(*local_slices(q, k, v, s), cfg)
+            parts.append(o)
+            comps.append(c)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.cat(parts), full)
+        assert torch.equal(torch.cat(comps), comp)
