@@ -1,24 +1,20 @@
 // Fast path (AA_BF16): hand-written sm_100a kernels for b_q = b_kv = 128,
 // d = 128.
 //
-//   K1 anchor   fa_tiles<ANCHOR>  tile list {0} ∪ [wsb(g), qb]   (Alg. 1)
-//   K2 identify k_identify_fast   pooled-q · K, threshold, ballot (Alg. 2)
-//   K3 sparse   fa_tiles<SPARSE>  gathered stripe tiles (TMA gather4),
-//                                  merged with the K1 state       (Alg. 3)
-//   D  dense    fa_tiles<DENSE>   tiles 0..qb (causal baseline)
+//   K1 anchor   fa_pair<ANCHOR>  tile list {0} ∪ [wsb(g), qb]          (Alg. 1)
+//   K2 identify k_identify_tc    pooled-q · K on tcgen05, threshold  (Alg. 2)
+//   K3 sparse   fa_pair<SPARSE>  gathered stripe tiles (TMA gather4),
+//                                merged with the K1 state             (Alg. 3)
+//   D  dense    fa_pair<DENSE>   tiles 0..qb (causal baseline)
 //
-// fa_tiles: one CTA = one (head, 128-row query block); 6 warps:
-//   warp 0   TMA producer (Q once; K/V tile per iteration; gather4 for K3)
-//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5  softmax / epilogue: thread <-> query row (TMEM lane)
-// TMEM (256 cols): S = Q K^T (f32) in cols [0,128), P (f16, aliasing S cols
-// [0,64)) feeds O += P V from TMEM, O (f32) in cols [128,256).  96 KB smem
-// and 256 TMEM columns per CTA -> two co-resident CTAs per SM, so one CTA's
-// MMAs overlap the other's softmax.  Softmax is exp2-based with lazy
-// rescaling (O/l only rescaled when the running max grows by > 8 in log2
-// units); the state written out is exact (rescaled to the true max).
-// PV runs in f16 (P in [0, 256] keeps 11 mantissa bits; V converted
-// bf16 -> f16 once, exact for |v| in the f16 normal range).
+// fa_pair (see its comment): one CTA = two 128-row query blocks of one head
+// sharing every K/V tile; TMA producer warp, single-thread tcgen05 issuer,
+// two softmax warpgroups ping-ponging on the tensor pipe; S/P/O in TMEM.
+// Softmax is exp2-based with lazy rescaling (O/l rescaled only when the
+// running max grows by > 8 in log2 units); the state written out is exact
+// (rescaled to the true max).  PV runs in f16 (P in [0, 256] keeps 11
+// mantissa bits; V converted bf16 -> f16 once, exact for |v| in the f16
+// normal range).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -39,7 +35,8 @@ using namespace sm100;
 
 constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
-constexpr int kThreads = 192;
+constexpr int kThreads = 192;       // K2 identify CTA
+constexpr int kPairThreads = 384;   // fa_pair CTA
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -75,15 +72,16 @@ struct FaParams {
     int out_bf16;
 };
 
-struct Smem {
-    // 1024-byte aligned tiles (SWIZZLE_128B atoms)
-    uint8_t q[kTileBytes];
-    uint8_t k[kTileBytes];
-    uint8_t v[kTileBytes];
-    uint64_t bar_q, bar_k_full, bar_k_empty, bar_v_full, bar_v_empty, bar_s_full, bar_p_full,
-        bar_o_done;
+// Shared memory of fa_pair: two query tiles, 2-stage K and V rings.
+struct PairSmem {
+    uint8_t q[2][kTileBytes];
+    uint8_t k[2][kTileBytes];
+    uint8_t v[2][kTileBytes];
+    uint64_t bar_q;
+    uint64_t bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
+    uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
-    float red[4];
+    float red[2][4];
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
@@ -91,70 +89,93 @@ __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
     return it == 0 ? 0 : wsb + it - 1;  // ANCHOR: {0} then [wsb, qb]
 }
 
+// One CTA = two query blocks (A = qb, B = qb + 1) of one head and one group;
+// they share every K/V tile (and for K3 the same gathered stripe rows), so
+// each tile is loaded once for 256 query rows.  12 warps:
+//   warp 0      TMA producer (Q pair once; K and V through 2-stage rings)
+//   warp 1      TMEM allocator (512 columns) + single-thread MMA issuer
+//   warps 4-7   softmax / epilogue of query tile A   (TMEM lanes 0..127)
+//   warps 8-11  softmax / epilogue of query tile B
+// TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512); P_X is written
+// as f16 over S_X columns [0,64) and consumed from TMEM by O_X += P_X V.
+// MMA order per tile j:  PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1) — the tensor
+// pipe works on one tile's MMAs while the other tile's softmax runs (FA4-style
+// ping-pong); tcgen05 MMAs of one thread execute in issue order, so QK_X(j+1)
+// overwriting S_X after PV_X(j) has read P_X is ordered by the pipe.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
-    fa_tiles(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKg,
-             const __grid_constant__ CUtensorMap tmVg, const FaParams P) {
+__global__ void __launch_bounds__(kPairThreads, 1)
+    fa_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKg,
+            const __grid_constant__ CUtensorMap tmVg, const FaParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                       ~uintptr_t(1023));
+    PairSmem& S = *reinterpret_cast<PairSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // heavy-first: the last query blocks (longest tile lists) launch first
-    const int bid = blockIdx.x;
-    const int qb = P.T_m - 1 - bid / P.hq;
-    const int h = bid % P.hq;
+    // work item: heavy-first (last groups, last pairs first)
+    const int ipg = (P.step + 1) / 2;  // query-block pairs per group
+    const int L = blockIdx.x;
+    const int gi = P.groups - 1 - L / (ipg * P.hq);
+    const int rem = L % (ipg * P.hq);
+    const int pi = ipg - 1 - rem / P.hq;
+    const int h = rem % P.hq;
     const int kvh = h / P.rep;
-    const int g = qb / P.step;
+    const int qA = gi * P.step + 2 * pi;
+    if (qA >= P.T_m) return;
+    const bool hasB = (2 * pi + 1 < P.step) && (qA + 1 < P.T_m);
+    const int qB = qA + 1;
 
-    // tile list
-    int ntiles = 0, wsb = 0, count = 0;
+    int nA = 0, nB = 0, wsb = 0, count = 0;
     const uint32_t* list = nullptr;
     if (MODE == DENSE) {
-        ntiles = qb + 1;
+        nA = qA + 1;
+        nB = hasB ? qB + 1 : 0;
     } else if (MODE == ANCHOR) {
-        const int rb = g * P.step * kB;
+        const int rb = gi * P.step * kB;
         wsb = rb < 2 * kB ? 1 : rb / kB - 1;
-        ntiles = 1 + (qb >= wsb ? qb - wsb + 1 : 0);
+        nA = 1 + (qA >= wsb ? qA - wsb + 1 : 0);
+        nB = hasB ? 1 + (qB - wsb + 1) : 0;
     } else {
-        count = P.counts[h * P.groups + g];
-        list = P.csr ? P.idx + P.offsets[h * P.groups + g] : P.idx + h * P.cap + P.offsets[g];
-        ntiles = (count + kB - 1) / kB;
+        count = P.counts[h * P.groups + gi];
+        list = P.csr ? P.idx + P.offsets[h * P.groups + gi] : P.idx + h * P.cap + P.offsets[gi];
+        nA = (count + kB - 1) / kB;
+        nB = hasB ? nA : 0;
     }
+    const int ntiles = nA > nB ? nA : nB;
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
-        mbar_init(&S.bar_k_full, 1);
-        mbar_init(&S.bar_k_empty, 1);
-        mbar_init(&S.bar_v_full, 1);
-        mbar_init(&S.bar_v_empty, 1);
-        mbar_init(&S.bar_s_full, 1);
-        mbar_init(&S.bar_p_full, 128);
-        mbar_init(&S.bar_o_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&S.bar_k_full[b], 1);
+            mbar_init(&S.bar_k_empty[b], 1);
+            mbar_init(&S.bar_v_full[b], 1);
+            mbar_init(&S.bar_v_empty[b], 1);
+            mbar_init(&S.bar_s_full[b], 1);
+            mbar_init(&S.bar_p_full[b], 128);
+            mbar_init(&S.bar_o_done[b], 1);
+        }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&S.tmem_base, 256);
+    if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
-    const uint32_t tS = tmem;        // S / P
-    const uint32_t tO = tmem + 128;  // O
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0 && ntiles > 0) {
-            mbar_expect_tx(&S.bar_q, kTileBytes);
-            tma_load_3d(S.q, &tmQ, &S.bar_q, 0, qb * kB, h);
-            tma_load_3d(S.q + kAtomBytes, &tmQ, &S.bar_q, 64, qb * kB, h);
+            mbar_expect_tx(&S.bar_q, hasB ? 2 * kTileBytes : kTileBytes);
+            tma_load_3d(S.q[0], &tmQ, &S.bar_q, 0, qA * kB, h);
+            tma_load_3d(S.q[0] + kAtomBytes, &tmQ, &S.bar_q, 64, qA * kB, h);
+            if (hasB) {
+                tma_load_3d(S.q[1], &tmQ, &S.bar_q, 0, qB * kB, h);
+                tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
+            }
         }
         if (MODE == SPARSE) {
-            // Every lane gathers 4 of the tile's 128 rows (gather4 x 2 column
-            // halves, for K and for V), so a tile is 4 TMA issues per lane
-            // instead of 128 from one thread.  The next tile's indices are
-            // fetched while this tile's loads are in flight.
+            // every lane gathers 4 of a tile's 128 rows (gather4 x 2 column halves)
             auto fetch = [&](int t, int (&j)[4]) {
                 const int base = t * kB;
 #pragma unroll
@@ -166,41 +187,43 @@ __global__ void __launch_bounds__(kThreads, 2)
             int j[4];
             if (ntiles > 0) fetch(0, j);
             const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
-            uint8_t* kdst = S.k + lane * 4 * 128;
-            uint8_t* vdst = S.v + lane * 4 * 128;
             for (int it = 0; it < ntiles; ++it) {
+                const int st = it & 1;
                 int rk[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) rk[u] = kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
                 if (lane == 0) {
-                    if (it > 0) mbar_wait(&S.bar_k_empty, (it - 1) & 1);
-                    mbar_expect_tx(&S.bar_k_full, kTileBytes);
+                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
                 }
                 __syncwarp();
-                tma_gather4(kdst, &tmKg, &S.bar_k_full, 0, rk[0], rk[1], rk[2], rk[3]);
-                tma_gather4(kdst + kAtomBytes, &tmKg, &S.bar_k_full, 64, rk[0], rk[1], rk[2], rk[3]);
+                uint8_t* kd = S.k[st] + lane * 4 * 128;
+                tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
+                tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1], rk[2], rk[3]);
                 if (lane == 0) {
-                    if (it > 0) mbar_wait(&S.bar_v_empty, (it - 1) & 1);
-                    mbar_expect_tx(&S.bar_v_full, kTileBytes);
+                    if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
                 }
                 __syncwarp();
-                tma_gather4(vdst, &tmVg, &S.bar_v_full, 0, vh + j[0], vh + j[1], vh + j[2], vh + j[3]);
-                tma_gather4(vdst + kAtomBytes, &tmVg, &S.bar_v_full, 64, vh + j[0], vh + j[1],
+                uint8_t* vd = S.v[st] + lane * 4 * 128;
+                tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1], vh + j[2], vh + j[3]);
+                tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0], vh + j[1],
                             vh + j[2], vh + j[3]);
                 if (it + 1 < ntiles) fetch(it + 1, j);
             }
         } else {
             for (int it = 0; it < ntiles; ++it) {
                 if (lane == 0) {
+                    const int st = it & 1;
                     const int kt = kv_tile_of(MODE, it, wsb);
-                    if (it > 0) mbar_wait(&S.bar_k_empty, (it - 1) & 1);
-                    mbar_expect_tx(&S.bar_k_full, kTileBytes);
-                    tma_load_3d(S.k, &tmK, &S.bar_k_full, 0, kt * kB, kvh);
-                    tma_load_3d(S.k + kAtomBytes, &tmK, &S.bar_k_full, 64, kt * kB, kvh);
-                    if (it > 0) mbar_wait(&S.bar_v_empty, (it - 1) & 1);
-                    mbar_expect_tx(&S.bar_v_full, kTileBytes);
-                    tma_load_3d(S.v, &tmV, &S.bar_v_full, 0, kt * kB, kvh);
-                    tma_load_3d(S.v + kAtomBytes, &tmV, &S.bar_v_full, 64, kt * kB, kvh);
+                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
+                    tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
+                    tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
+                    if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
+                    tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
+                    tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
                 }
                 __syncwarp();
             }
@@ -208,236 +231,258 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0 && ntiles > 0) {
-            const uint32_t q0 = smem_u32(S.q), k0 = smem_u32(S.k), v0 = smem_u32(S.v);
-            mbar_wait(&S.bar_q, 0);
-            for (int it = 0; it < ntiles; ++it) {
-                mbar_wait(&S.bar_k_full, it & 1);
-                if (it > 0) mbar_wait(&S.bar_o_done, (it - 1) & 1);  // P(it-1) consumed
+            const uint32_t qa0 = smem_u32(S.q[0]), qb0 = smem_u32(S.q[1]);
+            auto qk = [&](int X, int j) {
+                const int st = j & 1;
+                mbar_wait(&S.bar_k_full[st], (j >> 1) & 1);
                 tc_fence_after();
+                const uint32_t q0 = X ? qb0 : qa0, k0 = smem_u32(S.k[st]);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-                    mma_ss(tS, sdesc_sw128(q0 + off, 16, 1024), sdesc_sw128(k0 + off, 16, 1024),
-                           kIdescQK, kk > 0 ? 1u : 0u);
+                    mma_ss(tmem + X * 128, sdesc_sw128(q0 + off, 16, 1024),
+                           sdesc_sw128(k0 + off, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
                 }
-                mma_commit(&S.bar_s_full);
-                mma_commit(&S.bar_k_empty);
-                mbar_wait(&S.bar_p_full, it & 1);
-                mbar_wait(&S.bar_v_full, it & 1);
+                mma_commit(&S.bar_s_full[X]);
+            };
+            auto pv = [&](int X, int j) {
+                const int st = j & 1;
+                mbar_wait(&S.bar_p_full[X], j & 1);
+                mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 tc_fence_after();
+                const uint32_t v0 = smem_u32(S.v[st]);
+                const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
+                for (int kk = 0; kk < 8; ++kk)
                     mma_ts(tO, tS + kk * 8, sdesc_sw128(v0 + kk * 2048, kAtomBytes, 1024), kIdescPV,
-                           (it > 0 || kk > 0) ? 1u : 0u);
+                           (j > 0 || kk > 0) ? 1u : 0u);
+                mma_commit(&S.bar_o_done[X]);
+            };
+            mbar_wait(&S.bar_q, 0);
+            if (nA > 0) qk(0, 0);
+            if (nB > 0) qk(1, 0);
+            mma_commit(&S.bar_k_empty[0]);
+            for (int j = 0; j < ntiles; ++j) {
+                if (j < nA) {
+                    pv(0, j);
+                    if (j + 1 < nA) qk(0, j + 1);
                 }
-                mma_commit(&S.bar_o_done);
-                mma_commit(&S.bar_v_empty);
+                if (j < nB) {
+                    pv(1, j);
+                    if (j + 1 < nB) qk(1, j + 1);
+                }
+                mma_commit(&S.bar_v_empty[j & 1]);
+                if (j + 1 < ntiles) mma_commit(&S.bar_k_empty[(j + 1) & 1]);
             }
         }
         __syncwarp();
-    } else {
+    } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax
-        const int quad = warp & 3;                 // TMEM lane quadrant of this warp
-        const int r = quad * 32 + lane;            // row within the query block
-        const int row = qb * kB + r;               // global query row
-        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const float c = P.scale_log2;
-        float m_used = -INFINITY;  // running max, log2 units (lazy)
-        float m_raw = -INFINITY;   // true max of raw q.k
-        float l = 0.f;
+        const int X = warp >= 8 ? 1 : 0;
+        const int nX = X ? nB : nA;
+        const int qx = X ? qB : qA;
+        if (X == 1 && !hasB) {
+            // no second query block in this item
+        } else {
+            const int quad = warp & 3;
+            const int r = quad * 32 + lane;
+            const int row = qx * kB + r;
+            const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+            const uint32_t tS = tmem + X * 128 + lane_off;
+            const uint32_t tO = tmem + 256 + X * 128 + lane_off;
+            const float c = P.scale_log2;
+            float m_used = -INFINITY;  // running max, log2 units (lazy)
+            float m_raw = -INFINITY;   // true max of raw q.k
+            float l = 0.f;
 
-        for (int it = 0; it < ntiles; ++it) {
-            // valid key columns of this tile for this row
-            int lim;
-            if (MODE == SPARSE) {
-                lim = min(kB, count - it * kB);
-            } else {
-                const int kt = kv_tile_of(MODE, it, wsb);
-                lim = min(kB, P.n - kt * kB);
-                if (kt == qb) lim = min(lim, r + 1);
-            }
-            mbar_wait(&S.bar_s_full, it & 1);
-            tc_fence_after();
-            // pass 1: row max
-            float mx = -INFINITY;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tS + lane_off + ch * 32, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (ch * 32 + j < lim) mx = fmaxf(mx, __uint_as_float(v[j]));
-            }
-            m_raw = fmaxf(m_raw, mx);
-            const float mx2 = mx * c;
-            bool rescale = false;
-            float alpha = 1.f;
-            if (mx2 > m_used + 8.f) {
-                alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx2);
-                m_used = mx2;
-                rescale = it > 0;
-            }
-            l *= alpha;
-            const float base = (m_used == -INFINITY) ? 0.f : m_used;
-            // pass 2: P = 2^(s*c - m) as f16, written over S cols [0, 64)
-            float lsum = 0.f;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tS + lane_off + ch * 32, v);
-                tmem_wait_ld();
-                uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                    const int col = ch * 32 + j;
-                    const float p0 = col < lim ? ex2(fmaf(__uint_as_float(v[j]), c, -base)) : 0.f;
-                    const float p1 = col + 1 < lim ? ex2(fmaf(__uint_as_float(v[j + 1]), c, -base)) : 0.f;
-                    lsum += p0 + p1;
-                    pk[j >> 1] = pack_half2(p0, p1);
+            for (int it = 0; it < nX; ++it) {
+                int lim;
+                if (MODE == SPARSE) {
+                    lim = min(kB, count - it * kB);
+                } else {
+                    const int kt = kv_tile_of(MODE, it, wsb);
+                    lim = min(kB, P.n - kt * kB);
+                    if (kt == qx) lim = min(lim, r + 1);
                 }
-                tmem_st16(tS + lane_off + ch * 16, pk);
-            }
-            l += lsum;
-            if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective
-                if (!rescale) alpha = 1.f;
+                mbar_wait(&S.bar_s_full[X], it & 1);
+                tc_fence_after();
+                float mx = -INFINITY;
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) {
                     uint32_t v[32];
-                    tmem_ld32(tO + lane_off + ch * 32, v);
+                    tmem_ld32(tS + ch * 32, v);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
-                    tmem_st32(tO + lane_off + ch * 32, v);
+                    for (int jj = 0; jj < 32; ++jj)
+                        if (ch * 32 + jj < lim) mx = fmaxf(mx, __uint_as_float(v[jj]));
                 }
+                m_raw = fmaxf(m_raw, mx);
+                const float mx2 = mx * c;
+                bool rescale = false;
+                float alpha = 1.f;
+                if (mx2 > m_used + 8.f) {
+                    alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx2);
+                    m_used = mx2;
+                    rescale = it > 0;
+                }
+                l *= alpha;
+                const float base = (m_used == -INFINITY) ? 0.f : m_used;
+                float lsum = 0.f;
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tS + ch * 32, v);
+                    tmem_wait_ld();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int jj = 0; jj < 32; jj += 2) {
+                        const int col = ch * 32 + jj;
+                        const float p0 = col < lim ? ex2(fmaf(__uint_as_float(v[jj]), c, -base)) : 0.f;
+                        const float p1 =
+                            col + 1 < lim ? ex2(fmaf(__uint_as_float(v[jj + 1]), c, -base)) : 0.f;
+                        lsum += p0 + p1;
+                        pk[jj >> 1] = pack_half2(p0, p1);
+                    }
+                    tmem_st16(tS + ch * 16, pk);
+                }
+                l += lsum;
+                if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective
+                    if (!rescale) alpha = 1.f;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld32(tO + ch * 32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            v[jj] = __float_as_uint(__uint_as_float(v[jj]) * alpha);
+                        tmem_st32(tO + ch * 32, v);
+                    }
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&S.bar_p_full[X]);
             }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&S.bar_p_full);
-        }
 
-        // ------------------------------------------------------------ epilogue
-        if (ntiles > 0) {
-            mbar_wait(&S.bar_o_done, (ntiles - 1) & 1);
-            tc_fence_after();
-        }
-        const bool valid_row = row < P.n;
-        const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
-        if (MODE == ANCHOR) {
-            const float mt2 = m_raw * c;
-            const float f = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
-            float* acc = P.acc_out + rowoff;
+            // -------------------------------------------------------- epilogue
+            if (nX > 0) {
+                mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
+                tc_fence_after();
+            }
+            const bool valid_row = row < P.n;
+            const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
+            if (MODE == ANCHOR) {
+                const float mt2 = m_raw * c;
+                const float f = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
+                float* acc = P.acc_out + rowoff;
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tO + lane_off + ch * 32, v);
-                tmem_wait_ld();
-                if (valid_row) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 o;
-                        o.x = __uint_as_float(v[j]) * f;
-                        o.y = __uint_as_float(v[j + 1]) * f;
-                        o.z = __uint_as_float(v[j + 2]) * f;
-                        o.w = __uint_as_float(v[j + 3]) * f;
-                        *reinterpret_cast<float4*>(acc + ch * 32 + j) = o;
-                    }
-                }
-            }
-            const float m_nat = m_raw * P.inv_sqrt_d;
-            if (valid_row) {
-                P.m_out[static_cast<size_t>(h) * P.n + row] = m_nat;
-                P.l_out[static_cast<size_t>(h) * P.n + row] = l * f;
-            }
-            // per-query-block partial sums for pooling (Alg. 2 inputs)
-            if (P.msum != nullptr) {
-                float ms = valid_row ? m_nat : 0.f;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
-                if (lane == 0) S.red[quad] = ms;
-            }
-            if (P.qsum != nullptr) {
-                // column r of the Q tile, summed over its 128 rows (zero-filled past n)
-                const int col = r;
-                const uint8_t* atom = S.q + (col >> 6) * kAtomBytes;
-                const int chunk = (col & 63) >> 3, e = col & 7;
-                float s = 0.f;
-                for (int rr = 0; rr < kB; ++rr) {
-                    const __nv_bfloat16 x = *reinterpret_cast<const __nv_bfloat16*>(
-                        atom + rr * 128 + ((chunk ^ (rr & 7)) << 4) + e * 2);
-                    s += __bfloat162float(x);
-                }
-                P.qsum[(static_cast<size_t>(h) * P.T_m + qb) * kD + col] = s;
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (P.msum != nullptr && threadIdx.x == 64) {
-                P.msum[static_cast<size_t>(h) * P.T_m + qb] =
-                    static_cast<double>(S.red[0]) + S.red[1] + S.red[2] + S.red[3];
-            }
-        } else {
-            // O = O_tiles / l  (DENSE)  or merged with the anchor state (SPARSE)
-            float fa = 0.f, fs = 1.f, inv = 0.f;
-            const float* acc_a = nullptr;
-            if (MODE == SPARSE) {
-                const float ma = valid_row ? P.m_in[static_cast<size_t>(h) * P.n + row] : 0.f;
-                const float la = valid_row ? P.l_in[static_cast<size_t>(h) * P.n + row] : 1.f;
-                const float ma2 = ma * kLog2e;
-                const float M = fmaxf(ma2, m_used);
-                fa = ex2(ma2 - M);
-                fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
-                inv = 1.f / (la * fa + l * fs);
-                acc_a = P.acc_in + rowoff;
-            } else {
-                inv = 1.f / l;
-            }
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t v[32];
-                if (ntiles > 0) {
-                    tmem_ld32(tO + lane_off + ch * 32, v);
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tO + ch * 32, v);
                     tmem_wait_ld();
-                } else {
+                    if (valid_row) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = 0u;
+                        for (int jj = 0; jj < 32; jj += 4)
+                            *reinterpret_cast<float4*>(acc + ch * 32 + jj) = make_float4(
+                                __uint_as_float(v[jj]) * f, __uint_as_float(v[jj + 1]) * f,
+                                __uint_as_float(v[jj + 2]) * f, __uint_as_float(v[jj + 3]) * f);
+                    }
+                    __syncwarp();
                 }
+                const float m_nat = m_raw * P.inv_sqrt_d;
                 if (valid_row) {
-                float o[32];
+                    P.m_out[static_cast<size_t>(h) * P.n + row] = m_nat;
+                    P.l_out[static_cast<size_t>(h) * P.n + row] = l * f;
+                }
+                if (P.msum != nullptr) {
+                    float ms = valid_row ? m_nat : 0.f;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(v[j]) * fs;
+                    for (int o = 16; o; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
+                    if (lane == 0) S.red[X][quad] = ms;
+                }
+                if (P.qsum != nullptr) {
+                    // column r of this query tile, summed over its 128 rows (zero past n)
+                    const int col = r;
+                    const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes;
+                    const int chunk = (col & 63) >> 3, e = col & 7;
+                    float s = 0.f;
+                    for (int rr = 0; rr < kB; ++rr) {
+                        const __nv_bfloat16 x = *reinterpret_cast<const __nv_bfloat16*>(
+                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4) + e * 2);
+                        s += __bfloat162float(x);
+                    }
+                    P.qsum[(static_cast<size_t>(h) * P.T_m + qx) * kD + col] = s;
+                }
+                if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+                else asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (P.msum != nullptr && quad == 0 && lane == 0) {
+                    P.msum[static_cast<size_t>(h) * P.T_m + qx] =
+                        static_cast<double>(S.red[X][0]) + S.red[X][1] + S.red[X][2] + S.red[X][3];
+                }
+            } else {
+                float fa = 0.f, fs = 1.f, inv = 0.f;
+                const float* acc_a = nullptr;
                 if (MODE == SPARSE) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(acc_a + ch * 32 + j);
-                        o[j] += a.x * fa;
-                        o[j + 1] += a.y * fa;
-                        o[j + 2] += a.z * fa;
-                        o[j + 3] += a.w * fa;
-                    }
-                }
-                if (P.out_bf16) {
-                    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(P.out) + rowoff + ch * 32;
-#pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 w;
-                        __nv_bfloat162 t0 = __floats2bfloat162_rn(o[j] * inv, o[j + 1] * inv);
-                        __nv_bfloat162 t1 = __floats2bfloat162_rn(o[j + 2] * inv, o[j + 3] * inv);
-                        __nv_bfloat162 t2 = __floats2bfloat162_rn(o[j + 4] * inv, o[j + 5] * inv);
-                        __nv_bfloat162 t3 = __floats2bfloat162_rn(o[j + 6] * inv, o[j + 7] * inv);
-                        w.x = *reinterpret_cast<uint32_t*>(&t0);
-                        w.y = *reinterpret_cast<uint32_t*>(&t1);
-                        w.z = *reinterpret_cast<uint32_t*>(&t2);
-                        w.w = *reinterpret_cast<uint32_t*>(&t3);
-                        *reinterpret_cast<uint4*>(out + j) = w;
-                    }
+                    const float ma = valid_row ? P.m_in[static_cast<size_t>(h) * P.n + row] : 0.f;
+                    const float la = valid_row ? P.l_in[static_cast<size_t>(h) * P.n + row] : 1.f;
+                    const float ma2 = ma * kLog2e;
+                    const float M = fmaxf(ma2, m_used);
+                    fa = ex2(ma2 - M);
+                    fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
+                    inv = 1.f / (la * fa + l * fs);
+                    acc_a = P.acc_in + rowoff;
                 } else {
-                    float* out = static_cast<float*>(P.out) + rowoff + ch * 32;
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(out + j) =
-                            make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
+                    inv = 1.f / l;
                 }
-                }  // valid_row
-                __syncwarp();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    if (nX > 0) {
+                        tmem_ld32(tO + ch * 32, v);
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) v[jj] = 0u;
+                    }
+                    if (valid_row) {
+                        float o[32];
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) o[jj] = __uint_as_float(v[jj]) * fs;
+                        if (MODE == SPARSE) {
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 4) {
+                                const float4 a = *reinterpret_cast<const float4*>(acc_a + ch * 32 + jj);
+                                o[jj] += a.x * fa;
+                                o[jj + 1] += a.y * fa;
+                                o[jj + 2] += a.z * fa;
+                                o[jj + 3] += a.w * fa;
+                            }
+                        }
+                        if (P.out_bf16) {
+                            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(P.out) + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 8) {
+                                uint4 w;
+                                __nv_bfloat162 t0 = __floats2bfloat162_rn(o[jj] * inv, o[jj + 1] * inv);
+                                __nv_bfloat162 t1 = __floats2bfloat162_rn(o[jj + 2] * inv, o[jj + 3] * inv);
+                                __nv_bfloat162 t2 = __floats2bfloat162_rn(o[jj + 4] * inv, o[jj + 5] * inv);
+                                __nv_bfloat162 t3 = __floats2bfloat162_rn(o[jj + 6] * inv, o[jj + 7] * inv);
+                                w.x = *reinterpret_cast<uint32_t*>(&t0);
+                                w.y = *reinterpret_cast<uint32_t*>(&t1);
+                                w.z = *reinterpret_cast<uint32_t*>(&t2);
+                                w.w = *reinterpret_cast<uint32_t*>(&t3);
+                                *reinterpret_cast<uint4*>(out + jj) = w;
+                            }
+                        } else {
+                            float* out = static_cast<float*>(P.out) + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 4)
+                                *reinterpret_cast<float4*>(out + jj) = make_float4(
+                                    o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
+                        }
+                    }
+                    __syncwarp();
+                }
             }
         }
     }
@@ -445,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, 256);
+    if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------------------ K2
@@ -737,7 +782,7 @@ cudaError_t make_map_gather(CUtensorMap* m, const void* base, CUtensorMapDataTyp
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+constexpr size_t kSmemBytes = sizeof(PairSmem) + 1024;
 
 template <int MODE>
 cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const void* v16,
@@ -763,13 +808,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     P.kv_row_rows = static_cast<int>(f.kv_rs / kD);
     static bool attr_set[3] = {false, false, false};
     if (!attr_set[MODE]) {
-        if ((e = cudaFuncSetAttribute(fa_tiles<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if ((e = cudaFuncSetAttribute(fa_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kSmemBytes))))
             return e;
         attr_set[MODE] = true;
     }
-    const unsigned grid = static_cast<unsigned>(P.T_m * f.hq);
-    fa_tiles<MODE><<<grid, kThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
+    const unsigned grid = static_cast<unsigned>(P.groups * ((P.step + 1) / 2) * f.hq);
+    fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
     return cudaGetLastError();
 }
 
