@@ -113,13 +113,16 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // work item: heavy-first (last groups, last pairs first)
+    // work item: heavy-first (last groups first).  Within a group, the pairs of
+    // one head are adjacent, then the heads of one KV head: CTAs that run
+    // together gather the same stripe rows (one list per (head, group); GQA
+    // siblings select mostly the same keys), so the gathers hit L2.
     const int ipg = (P.step + 1) / 2;  // query-block pairs per group
     const int L = blockIdx.x;
     const int gi = P.groups - 1 - L / (ipg * P.hq);
     const int rem = L % (ipg * P.hq);
-    const int pi = ipg - 1 - rem / P.hq;
-    const int h = rem % P.hq;
+    const int h = rem / ipg;
+    const int pi = ipg - 1 - rem % ipg;
     const int kvh = h / P.rep;
     const int qA = gi * P.step + 2 * pi;
     if (qA >= P.T_m) return;
