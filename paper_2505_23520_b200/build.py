@@ -28,6 +28,7 @@ CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+NVCC_FLAGS += os.environ.get("AA_NVCC_EXTRA", "").split()  # developer experiments only
 
 CAPI_LIB = os.path.join(LIB, "libanchorattn_b200.so")
 CPP_LIB = os.path.join(LIB, "libanchorattn_cpp.so")

@@ -70,6 +70,7 @@ struct FaParams {
     // SPARSE / DENSE output
     void* out;
     int out_bf16;
+    int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
 };
 
 // Shared memory of fa_pair: two query tiles, 2-stage K and V rings.
@@ -147,13 +148,21 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     }
     const int ntiles = nA > nB ? nA : nB;
 
+    // K3 cluster mode (P.cluster = C > 1): the C CTAs of a cluster are C pairs
+    // of the same (head, group) and so walk the same gathered tiles; each CTA
+    // gathers 128/C rows of every tile and multicasts them to all C CTAs, and
+    // a K/V stage is refilled only after all C consumers released it.
+    const int C = MODE == SPARSE ? P.cluster : 1;
+    const uint32_t crank = C > 1 ? cluster_ctarank() : 0;
+    const uint16_t cmask = static_cast<uint16_t>((1u << C) - 1u);
+
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&S.bar_k_full[b], 1);
-            mbar_init(&S.bar_k_empty[b], 1);
+            mbar_init(&S.bar_k_empty[b], C);
             mbar_init(&S.bar_v_full[b], 1);
-            mbar_init(&S.bar_v_empty[b], 1);
+            mbar_init(&S.bar_v_empty[b], C);
             mbar_init(&S.bar_s_full[b], 1);
             mbar_init(&S.bar_p_full[b], 128);
             mbar_init(&S.bar_o_done[b], 1);
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     }
     if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
-    __syncthreads();
+    if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
 
@@ -178,13 +187,19 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
         if (MODE == SPARSE) {
-            // every lane gathers 4 of a tile's 128 rows (gather4 x 2 column halves)
+            // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
+            // column halves, for K and for V).  Standalone CTA: 32 lanes cover
+            // the 128 rows; in a cluster of C, this CTA covers rows
+            // [crank*128/C, (crank+1)*128/C) and multicasts them.
+            const int lanes = 32 / C;
+            const bool gl = lane < lanes;
+            const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
             auto fetch = [&](int t, int (&j)[4]) {
                 const int base = t * kB;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int e = base + lane * 4 + u;
-                    j[u] = static_cast<int>(list[e < count ? e : base]);
+                    const int e = base + row0 + u;
+                    j[u] = gl ? static_cast<int>(list[e < count ? e : base]) : 0;
                 }
             };
             int j[4];
@@ -200,18 +215,37 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
                 }
                 __syncwarp();
-                uint8_t* kd = S.k[st] + lane * 4 * 128;
-                tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
-                tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1], rk[2], rk[3]);
+                uint8_t* kd = S.k[st] + row0 * 128;
+                if (gl) {
+                    if (C > 1) {
+                        tma_gather4_mc(kd, &tmKg, &S.bar_k_full[st], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], cmask, 64, rk[0], rk[1],
+                                       rk[2], rk[3]);
+                    } else {
+                        tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1], rk[2],
+                                    rk[3]);
+                    }
+                }
                 if (lane == 0) {
                     if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                     mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
                 }
                 __syncwarp();
-                uint8_t* vd = S.v[st] + lane * 4 * 128;
-                tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1], vh + j[2], vh + j[3]);
-                tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0], vh + j[1],
-                            vh + j[2], vh + j[3]);
+                uint8_t* vd = S.v[st] + row0 * 128;
+                if (gl) {
+                    if (C > 1) {
+                        tma_gather4_mc(vd, &tmVg, &S.bar_v_full[st], cmask, 0, vh + j[0], vh + j[1],
+                                       vh + j[2], vh + j[3]);
+                        tma_gather4_mc(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], cmask, 64, vh + j[0],
+                                       vh + j[1], vh + j[2], vh + j[3]);
+                    } else {
+                        tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1], vh + j[2],
+                                    vh + j[3]);
+                        tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0], vh + j[1],
+                                    vh + j[2], vh + j[3]);
+                    }
+                }
                 if (it + 1 < ntiles) fetch(it + 1, j);
             }
         } else {
@@ -261,10 +295,14 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                            (j > 0 || kk > 0) ? 1u : 0u);
                 mma_commit(&S.bar_o_done[X]);
             };
+            // a stage is released to every producer of the cluster that fills it
+            auto release = [&](uint64_t* bar) {
+                if (C > 1) mma_commit_mc(bar, cmask); else mma_commit(bar);
+            };
             mbar_wait(&S.bar_q, 0);
             if (nA > 0) qk(0, 0);
             if (nB > 0) qk(1, 0);
-            mma_commit(&S.bar_k_empty[0]);
+            release(&S.bar_k_empty[0]);
             for (int j = 0; j < ntiles; ++j) {
                 if (j < nA) {
                     pv(0, j);
@@ -274,8 +312,15 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     pv(1, j);
                     if (j + 1 < nB) qk(1, j + 1);
                 }
-                mma_commit(&S.bar_v_empty[j & 1]);
-                if (j + 1 < ntiles) mma_commit(&S.bar_k_empty[(j + 1) & 1]);
+                release(&S.bar_v_empty[j & 1]);
+                if (j + 1 < ntiles) release(&S.bar_k_empty[(j + 1) & 1]);
+            }
+            if (C > 1) {
+                // every CTA's last releases have landed here before the exit
+                // cluster barrier, so no remote arrive can target a retired CTA
+                const int jl = ntiles - 1;
+                mbar_wait(&S.bar_k_empty[jl & 1], (jl >> 1) & 1);
+                mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
             }
         }
         __syncwarp();
@@ -491,7 +536,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
@@ -816,9 +861,36 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
             return e;
         attr_set[MODE] = true;
     }
-    const unsigned grid = static_cast<unsigned>(P.groups * ((P.step + 1) / 2) * f.hq);
-    fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
-    return cudaGetLastError();
+    const int ipg = (P.step + 1) / 2;
+    const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
+    // K3: cluster the pairs of one (head, group) so each gathered tile is
+    // fetched once per cluster (TMA multicast); needs every group complete
+    // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
+    P.cluster = 1;
+    if (MODE == SPARSE && P.T_m % P.step == 0) {
+        for (int c : {4, 2})
+            if (ipg % c == 0) {
+                P.cluster = c;
+                break;
+            }
+    }
+    if (P.cluster == 1) {
+        fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kPairThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(P.cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fa_pair<MODE>, tq, tk, tv, tkg, tvg, P);
 }
 
 cudaError_t convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s) {
