@@ -174,8 +174,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
-
+    // register split (per warpgroup, inside each role branch): the producer /
+    // MMA warpgroup needs few registers, the two softmax warpgroups hold a
+    // whole S row (128 f32) each.
     if (warp == 0) {
+        setmaxnreg_dec<56>();
         // ------------------------------------------------------------ producer
         if (lane == 0 && ntiles > 0) {
             mbar_expect_tx(&S.bar_q, hasB ? 2 * kTileBytes : kTileBytes);
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
     } else if (warp == 1) {
+        setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0 && ntiles > 0) {
             const uint32_t qa0 = smem_u32(S.q[0]), qb0 = smem_u32(S.q[1]);
@@ -324,7 +328,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp < 4) {
+        setmaxnreg_dec<56>();  // warps 2-3: no role, donate registers
+    } else {
+        setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
         const int nX = X ? nB : nA;
@@ -354,16 +361,19 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 mbar_wait(&S.bar_s_full[X], it & 1);
                 tc_fence_after();
-                float mx = -INFINITY;
+                // single pass: the whole S row in registers
+                uint32_t v[128];
+                tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
+                tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
+                tmem_wait_ld();
+                if (lim < kB) {  // causal diagonal / sequence tail / list tail
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t v[32];
-                    tmem_ld32(tS + ch * 32, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj)
-                        if (ch * 32 + jj < lim) mx = fmaxf(mx, __uint_as_float(v[jj]));
+                    for (int jj = 0; jj < kB; ++jj)
+                        if (jj >= lim) v[jj] = 0xff800000u;  // -inf -> p = 0
                 }
+                float mx = row_max128(v);
                 m_raw = fmaxf(m_raw, mx);
                 const float mx2 = mx * c;
                 bool rescale = false;
@@ -375,25 +385,22 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 l *= alpha;
                 const float base = (m_used == -INFINITY) ? 0.f : m_used;
-                float lsum = 0.f;
+                float2 lsum = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t v[32];
-                    tmem_ld32(tS + ch * 32, v);
-                    tmem_wait_ld();
                     uint32_t pk[16];
 #pragma unroll
                     for (int jj = 0; jj < 32; jj += 2) {
-                        const int col = ch * 32 + jj;
-                        const float p0 = col < lim ? ex2(fmaf(__uint_as_float(v[jj]), c, -base)) : 0.f;
-                        const float p1 =
-                            col + 1 < lim ? ex2(fmaf(__uint_as_float(v[jj + 1]), c, -base)) : 0.f;
-                        lsum += p0 + p1;
-                        pk[jj >> 1] = pack_half2(p0, p1);
+                        const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
+                                                           __uint_as_float(v[ch * 32 + jj + 1])),
+                                               c, -base);
+                        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+                        lsum = fadd2(lsum, pp);
+                        pk[jj >> 1] = pack_half2(pp.x, pp.y);
                     }
                     tmem_st16(tS + ch * 16, pk);
                 }
-                l += lsum;
+                l += lsum.x + lsum.y;
                 if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective
                     if (!rescale) alpha = 1.f;
 #pragma unroll

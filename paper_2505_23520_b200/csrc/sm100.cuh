@@ -83,6 +83,16 @@ __device__ __forceinline__ void tma_gather4_mc(void* dst, const CUtensorMap* m, 
         : "memory");
 }
 
+// ---- per-warpgroup register budget -------------------------------------------------
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ---- clusters -------------------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -206,6 +216,42 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+}
+
+// f32x2 SIMD (FFMA2 / FADD2) and 3-input max (FMNMX3) — sm_100 ALU forms.
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float c) {
+    uint64_t r;
+    const float2 bb = make_float2(b, b), cc = make_float2(c, c);
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&bb)),
+          "l"(*reinterpret_cast<const uint64_t*>(&cc)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// Max of 128 f32 bit patterns (a row of S) with a 3-input tree.
+__device__ __forceinline__ float row_max128(const uint32_t (&v)[128]) {
+    float m[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float a = __uint_as_float(v[q * 32]);
+#pragma unroll
+        for (int j = 1; j < 31; j += 2)
+            a = fmax3(a, __uint_as_float(v[q * 32 + j]), __uint_as_float(v[q * 32 + j + 1]));
+        m[q] = fmaxf(a, __uint_as_float(v[q * 32 + 31]));
+    }
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
 
 __device__ __forceinline__ float ex2(float x) {
