@@ -325,6 +325,27 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "work": f"4*d*positions = {kernels[dom]['flops']:.4e} FLOP per launch"}
 
+    # recall of the selection at 128k: one dense QK pass (RECALL kernel) over
+    # this rank's heads with the stripe lists of the timed configuration
+    recall = None
+    try:
+        st = capi.compute_anchor(q, k, v, cfg)
+        anchor, qbar = capi.pool(q, k, st, cfg)
+        idx, cnts = capi.identify(q, k, qbar, anchor, cfg)
+        del st
+        r = capi.union_recall(q, k, idx, cnts, cfg)
+        torch.cuda.synchronize()
+        rsum = float(r.sum().item())
+        if world > 1:
+            t = torch.tensor([rsum], device=dev, dtype=torch.float64)
+            dist.all_reduce(t)
+            rsum = float(t.item())
+        recall = rsum / args.hq
+        del idx, cnts
+    except Exception as exc:  # noqa: BLE001 - reported, not fatal
+        print(f"[bench] recall pass failed: {exc}", file=sys.stderr)
+    torch.cuda.empty_cache()
+
     # dense tcgen05 FlashAttention-style kernel on the same layer (baseline)
     dense_ms = None
     if not args.no_dense:
@@ -403,7 +424,7 @@ def run_ours(args):
                        "global_batch": 1, "seq_len": args.n,
                        "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (q/k/v 1.6 GB per layer), no flush"},
-            "sparsity": sparsity, "computed_positions": comp_total,
+            "sparsity": sparsity, "recall": recall, "computed_positions": comp_total,
             "stage_ms": dict(zip(capi.STAGES, stage_ms)),
             "kernels": kernels,
             "dense_ms_per_layer": dense_ms,

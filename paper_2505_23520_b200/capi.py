@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libanchorattn_b200.so")
+LIB_PATH = os.environ.get("AA_LIB_PATH") or os.path.join(PKG, "lib", "libanchorattn_b200.so")
 
 AA_F32, AA_BF16, AA_F64 = 0, 1, 2
 _STATUS = {0: "AA_OK", 1: "AA_ERR_INVALID_ARGUMENT", 2: "AA_ERR_OUT_OF_RANGE",

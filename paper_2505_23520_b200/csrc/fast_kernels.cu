@@ -42,8 +42,18 @@ constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
 constexpr uint32_t kIdescPV = idesc_f16(0, 0, 1, 128, 128);  // f16 x f16,  B MN-major
 constexpr float kLog2e = 1.4426950408889634f;
+// Exp2 pairs per 32 columns computed by ex2_poly2 on the FMA pipe instead of
+// MUFU.  Measured on B200 (128k Llama layer, profiles/README.md): 0 / 4 / 6 /
+// 8 pairs -> K3 18.6 / 19.2 / 19.5 / 20.0 ms — the softmax is issue-bound,
+// not MUFU-bound, so the offload is off.
+#ifndef AA_POLY_PAIRS
+#define AA_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = AA_POLY_PAIRS;
 
-enum Mode { ANCHOR = 0, SPARSE = 1, DENSE = 2 };
+// RECALL: the dense causal QK pass without PV, accumulating per row the
+// softmax mass of all keys and of the selected keys (covered ∪ stripes).
+enum Mode { ANCHOR = 0, SPARSE = 1, DENSE = 2, RECALL = 3 };
 
 struct FaParams {
     int n, hq, rep, T_m, step;
@@ -71,6 +81,10 @@ struct FaParams {
     void* out;
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
+    // RECALL inputs / output
+    const uint32_t* bits;   // selection bitmask [hq, G, words_per_row]
+    int64_t words_per_row;
+    double* row_recall;     // [hq, n]: selected / total softmax mass per row
 };
 
 // Shared memory of fa_pair: two query tiles, 2-stage K and V rings.
@@ -86,7 +100,7 @@ struct PairSmem {
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
-    if (mode == DENSE) return it;
+    if (mode == DENSE || mode == RECALL) return it;
     return it == 0 ? 0 : wsb + it - 1;  // ANCHOR: {0} then [wsb, qb]
 }
 
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
     int nA = 0, nB = 0, wsb = 0, count = 0;
     const uint32_t* list = nullptr;
-    if (MODE == DENSE) {
+    if (MODE == DENSE || MODE == RECALL) {
         nA = qA + 1;
         nB = hasB ? qB + 1 : 0;
     } else if (MODE == ANCHOR) {
@@ -260,10 +274,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
                     tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
                     tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
-                    if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
-                    mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
-                    tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
-                    tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
+                    if (MODE != RECALL) {
+                        if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                        mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
+                        tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
+                        tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
+                    }
                 }
                 __syncwarp();
             }
@@ -289,6 +305,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             auto pv = [&](int X, int j) {
                 const int st = j & 1;
                 mbar_wait(&S.bar_p_full[X], j & 1);
+                if (MODE == RECALL) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t v0 = smem_u32(S.v[st]);
@@ -349,6 +366,16 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             float m_used = -INFINITY;  // running max, log2 units (lazy)
             float m_raw = -INFINITY;   // true max of raw q.k
             float l = 0.f;
+            float l_sel = 0.f;         // RECALL: mass of the selected keys
+            // RECALL: this row group's stripe bitmask row and window start
+            const uint32_t* bits_x = nullptr;
+            int wstart_x = 0;
+            if (MODE == RECALL) {
+                bits_x = P.bits + (static_cast<int64_t>(h) * P.groups + gi) * P.words_per_row;
+                const int rb = gi * P.step * kB;
+                const int wsbx = rb < 2 * kB ? 1 : rb / kB - 1;
+                wstart_x = min(wsbx * kB, P.n);
+            }
 
             for (int it = 0; it < nX; ++it) {
                 int lim;
@@ -385,6 +412,35 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 l *= alpha;
                 const float base = (m_used == -INFINITY) ? 0.f : m_used;
+                if constexpr (MODE == RECALL) {
+                    // selected keys of this tile for this row's group: the initial
+                    // block and the local window are covered; middle keys are
+                    // selected iff their stripe bit is set
+                    l_sel *= alpha;
+                    const int kt = it;
+                    uint32_t sel[4] = {~0u, ~0u, ~0u, ~0u};
+                    if (kt > 0 && kt * kB < wstart_x) {
+                        const uint4 w = *reinterpret_cast<const uint4*>(bits_x + 4 * (kt - 1));
+                        sel[0] = w.x, sel[1] = w.y, sel[2] = w.z, sel[3] = w.w;
+                    }
+                    float2 la = make_float2(0.f, 0.f), ls = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int jj = 0; jj < kB; jj += 2) {
+                        const float2 x = ffma2(make_float2(__uint_as_float(v[jj]),
+                                                           __uint_as_float(v[jj + 1])),
+                                               c, -base);
+                        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+                        la = fadd2(la, pp);
+                        const uint32_t wd = sel[jj >> 5];
+                        ls = fadd2(ls, make_float2((wd >> (jj & 31)) & 1u ? pp.x : 0.f,
+                                                   (wd >> ((jj + 1) & 31)) & 1u ? pp.y : 0.f));
+                    }
+                    l += la.x + la.y;
+                    l_sel += ls.x + ls.y;
+                    tc_fence_before();
+                    mbar_arrive(&S.bar_p_full[X]);
+                    continue;
+                }
                 float2 lsum = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) {
@@ -394,7 +450,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
                                                            __uint_as_float(v[ch * 32 + jj + 1])),
                                                c, -base);
-                        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+                        // 12 of every 32 exponentials on the FMA pipe, the rest on
+                        // MUFU: balances the two pipes (MUFU alone needs as many
+                        // cycles per tile as the tensor core)
+                        const float2 pp = (jj >> 1) % 16 < kPolyPairs
+                                              ? ex2_poly2(x)
+                                              : make_float2(ex2(x.x), ex2(x.y));
                         lsum = fadd2(lsum, pp);
                         pk[jj >> 1] = pack_half2(pp.x, pp.y);
                     }
@@ -420,6 +481,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
 
             // -------------------------------------------------------- epilogue
+            if (MODE == RECALL) {
+                if (row < P.n)
+                    P.row_recall[static_cast<size_t>(h) * P.n + row] =
+                        static_cast<double>(l_sel) / static_cast<double>(l);
+            } else {
             if (nX > 0) {
                 mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
                 tc_fence_after();
@@ -539,6 +605,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     __syncwarp();
                 }
             }
+            }  // MODE != RECALL
         }
     }
 
@@ -765,6 +832,39 @@ __global__ void k_finalize_fast(int64_t total, int64_t d, const float* __restric
     }
 }
 
+// Capacity-layout (or CSR) stripe lists -> selection bitmask rows [hq, G, W]
+// (bit j - b_kv of row (h, g)); the RECALL pass reads these.
+__global__ void k_scatter_bits(Geo geo, const uint32_t* __restrict__ indices,
+                               const int32_t* __restrict__ counts,
+                               const int64_t* __restrict__ offsets, int64_t cap,
+                               uint32_t* __restrict__ bits, int64_t wpr) {
+    const int64_t g = blockIdx.x, h = blockIdx.y, G = gridDim.x;
+    const int64_t cnt = counts[h * G + g];
+    const uint32_t* list = indices + h * cap + offsets[g];
+    uint32_t* row = bits + (h * G + g) * wpr;
+    const int64_t lo = geo.b_kv, hi = geo.window_start(g);
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int64_t j = list[e];
+        if (j < lo || j >= hi) continue;  // covered keys count once (union_mask)
+        atomicOr(row + ((j - lo) >> 5), 1u << ((j - lo) & 31));
+    }
+}
+
+// recall[h] = mean over rows of the per-row captured mass (metrics.cpp:8-19).
+__global__ void k_recall_sum(int64_t n, const double* __restrict__ rows, double* __restrict__ recall) {
+    __shared__ double red[256];
+    const int64_t h = blockIdx.x;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += rows[h * n + i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) recall[h] = red[0] / static_cast<double>(n);
+}
+
 // V (bf16, strided) -> packed f16 [hkv, n, d] (exact for the f16 normal range).
 __global__ void k_v_to_f16(int64_t n, int64_t hkv, int64_t rs, int64_t hs,
                            const __nv_bfloat16* __restrict__ v, __half* __restrict__ v16) {
@@ -861,7 +961,7 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     P.scale_log2 = kLog2e * P.inv_sqrt_d;
     P.kv_head_rows = static_cast<int>(f.kv_hs / kD);
     P.kv_row_rows = static_cast<int>(f.kv_rs / kD);
-    static bool attr_set[3] = {false, false, false};
+    static bool attr_set[4] = {false, false, false, false};
     if (!attr_set[MODE]) {
         if ((e = cudaFuncSetAttribute(fa_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kSmemBytes))))
@@ -1013,9 +1113,33 @@ cudaError_t fast_dense(const FastArgs& f, const void* q, const void* k, const vo
     return launch_fa<DENSE>(f, q, k, v16, P, s);
 }
 
-cudaError_t fast_recall(const FastArgs&, const void*, const void*, const uint32_t*, const int32_t*,
-                        const int64_t*, int64_t, double*, double*, cudaStream_t) {
-    return cudaErrorNotSupported;
+cudaError_t fast_recall(const FastArgs& f, const void* q, const void* k, const uint32_t* indices,
+                        const int32_t* counts, const int64_t* offsets, int64_t cap,
+                        double* row_captured, double* recall, cudaStream_t s) {
+    const int64_t G = f.geo.groups();
+    const int64_t wpr = ((f.geo.n + 31) / 32 + 3) / 4 * 4;
+    const size_t bytes = static_cast<size_t>(f.hq * G * wpr) * 4;
+    void* bits = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync(&bits, bytes, s))) return e;
+    if ((e = cudaMemsetAsync(bits, 0, bytes, s))) {
+        cudaFreeAsync(bits, s);
+        return e;
+    }
+    k_scatter_bits<<<dim3(static_cast<unsigned>(G), static_cast<unsigned>(f.hq)), 256, 0, s>>>(
+        f.geo, indices, counts, offsets, cap, static_cast<uint32_t*>(bits), wpr);
+    FaParams P{};
+    P.bits = static_cast<const uint32_t*>(bits);
+    P.words_per_row = wpr;
+    P.row_recall = row_captured;
+    // RECALL loads no V: the V maps only need a valid address
+    e = launch_fa<RECALL>(f, q, k, k, P, s);
+    if (e == cudaSuccess) {
+        k_recall_sum<<<static_cast<unsigned>(f.hq), 256, 0, s>>>(f.geo.n, row_captured, recall);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(bits, s);
+    return e;
 }
 
 }  // namespace aa

@@ -235,6 +235,13 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
         : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
     return *reinterpret_cast<float2*>(&r);
 }
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.ftz.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -252,6 +259,37 @@ __device__ __forceinline__ float row_max128(const uint32_t (&v)[128]) {
         m[q] = fmaxf(a, __uint_as_float(v[q * 32 + 31]));
     }
     return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+
+__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+          "l"(*reinterpret_cast<const uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+// 2^x for two lanes on the FMA/ALU pipes instead of MUFU (FA4-style exp
+// offload).  x <= 8 here (lazy-max softmax), x may be -inf (masked column):
+// clamp to -125 so the exponent arithmetic cannot underflow; 2^-125 rounds to
+// 0 in the f16 P anyway.  Round-to-nearest split x = j + f, f in [-0.5, 0.5]
+// via the 1.5*2^23 trick; 2^f by a degree-3 fit (max rel. error 7.5e-5, below
+// the f16 half-ulp 2.4e-4 of P); 2^j added to the exponent bits.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+    const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));
+    const float2 f = fsub2(x, r);
+    float2 p = ffma2v(make_float2(0.05517113f, 0.05517113f), f, make_float2(0.24261008f, 0.24261008f));
+    p = ffma2v(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = ffma2v(p, f, make_float2(0.99992813f, 0.99992813f));
+    // (bits(t) << 23) == (j << 23) mod 2^32: the magic's low mantissa bits are 0
+    const uint32_t bx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+    const uint32_t by = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+    return make_float2(__uint_as_float(bx), __uint_as_float(by));
 }
 
 __device__ __forceinline__ float ex2(float x) {

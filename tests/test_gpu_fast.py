@@ -212,3 +212,23 @@ def test_stage_api_equals_fused_chain():
     torch.cuda.synchronize()
     assert torch.equal(comp, comp2)
     assert torch.equal(fused, out)
+
+
+@pytest.mark.parametrize("n,step,theta", [(4096, 16, 12.0), (2048, 2, 10.0), (3000, 4, 14.0)])
+def test_recall_pass_matches_oracle(oracle, n, step, theta):
+    """GPU recall (one dense QK pass keeping total and selected softmax mass per
+    row) == recall(union_mask(stripes), dense_probs) on the same stripe lists."""
+    c = capi()
+    q, k, v = gen(n, hq=2, hkv=1, seed=31 + n)
+    dq, dk, dv = q.cuda(), k.cuda(), v.cuda()
+    cfg = c.BlockConfig(128, 128, step, theta)
+    st = c.compute_anchor(dq, dk, dv, cfg)
+    anchor, qbar = c.pool(dq, dk, st, cfg)
+    idx, counts = c.identify(dq, dk, qbar, anchor, cfg)
+    rec = c.union_recall(dq, dk, idx, counts, cfg).cpu().numpy()
+    ocfg = Cfg(128, 128, step, theta)
+    for h in range(2):
+        ref = oracle.union_recall(q[h].float().numpy(), k[0].float().numpy(), ocfg,
+                                  idx[h].cpu().numpy().view(np.uint32),
+                                  counts[h].cpu().numpy().astype(np.int64))
+        assert abs(rec[h] - ref) <= 1e-4, (h, rec[h], ref)
