@@ -213,15 +213,33 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    # one process per GPU; if a test launches more ranks than GPUs, ranks share
+    # devices and the control collectives run over gloo instead of NCCL
+    local = local % ndev
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    host_group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=dev)
+            host_group = dist.new_group(backend="gloo")
+        else:
+            dist.init_process_group("gloo")
+
+    def reduce(vals, op="max"):
+        """Host scalars reduced over ranks (max for device-timed durations)."""
+        t = torch.tensor(vals, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM,
+                            group=host_group)
+        return t.tolist()
+
     if args.hkv % world:
         raise SystemExit(f"hkv={args.hkv} must be divisible by the rank count {world}")
     rep = args.hq // args.hkv
     kv_local = args.hkv // world
     kv0 = rank * kv_local
-    dev = torch.device("cuda", local)
 
     # this rank's KV heads and their query heads; each KV head is generated from
     # its own seed so the data does not depend on the rank count
@@ -276,15 +294,8 @@ def run_ours(args):
           flush=True)
     comp_local = int(computed.sum().item())
     covered, cand = layer_geometry(args.n, args.step_blocks)
-    if world > 1:
-        t = torch.tensor([ms_local], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        c = torch.tensor([comp_local], device=dev, dtype=torch.int64)
-        dist.all_reduce(c)
-        comp_total = int(c.item())
-    else:
-        ms, comp_total = ms_local, comp_local
+    ms = reduce([ms_local], "max")[0]
+    comp_total = int(reduce([comp_local], "sum")[0])
     causal = args.n * (args.n + 1) // 2
     sparsity = 1.0 - comp_total / (args.hq * causal)
 
@@ -335,11 +346,7 @@ def run_ours(args):
         del st
         r = capi.union_recall(q, k, idx, cnts, cfg)
         torch.cuda.synchronize()
-        rsum = float(r.sum().item())
-        if world > 1:
-            t = torch.tensor([rsum], device=dev, dtype=torch.float64)
-            dist.all_reduce(t)
-            rsum = float(t.item())
+        rsum = reduce([float(r.sum().item())], "sum")[0]
         recall = rsum / args.hq
         del idx, cnts
     except Exception as exc:  # noqa: BLE001 - reported, not fatal
@@ -360,12 +367,7 @@ def run_ours(args):
             capi.dense_attention(q, k, v, out=dout)
         b.record(stream)
         torch.cuda.synchronize()
-        dl = a.elapsed_time(b) / reps
-        if world > 1:
-            t = torch.tensor([dl], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dl = float(t.item())
-        dense_ms = dl
+        dense_ms = reduce([a.elapsed_time(b) / reps], "max")[0]
         del dout
 
     # e2e through the host-buffer C ABI entry (pinned host tensors)
@@ -385,17 +387,12 @@ def run_ours(args):
             tt = time.perf_counter()
             for _ in range(reps):
                 capi.anchor_attention_host(hq_h, hk, hv, cfg, out=o_h, computed=c_h)
-            e2e_ms = (time.perf_counter() - tt) * 1e3 / reps
-            if world > 1:
-                t = torch.tensor([e2e_ms], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                e2e_ms = float(t.item())
-            h2d = (hq_h.numel() + hk.numel() + hv.numel()) * 2
-            d2h = o_h.numel() * 4 + c_h.numel() * 8
-            if world > 1:
-                t = torch.tensor([h2d, d2h], device=dev, dtype=torch.int64)
-                dist.all_reduce(t)
-                h2d, d2h = int(t[0]), int(t[1])
+            # the host entry blocks until its own stream finishes: wall time of
+            # the call is the end-to-end latency (max over ranks)
+            e2e_ms = reduce([(time.perf_counter() - tt) * 1e3 / reps], "max")[0]
+            h2d, d2h = (int(x) for x in reduce(
+                [(hq_h.numel() + hk.numel() + hv.numel()) * 2, o_h.numel() * 4 + c_h.numel() * 8],
+                "sum"))
             e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h,
                    "path": "aa_anchor_attention_host (pinned host q/k/v -> device chain -> host out f32)"}
