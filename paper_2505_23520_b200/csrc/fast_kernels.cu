@@ -37,6 +37,12 @@ constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
 constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
+// fa_pair register split per warpgroup (setmaxnreg; 128*ctl + 256*softmax <= 64K)
+#ifndef AA_REGS_CTL
+#define AA_REGS_CTL 88
+#endif
+constexpr uint32_t kRegsCtl = AA_REGS_CTL;
+constexpr uint32_t kRegsSoftmax = (65536 / 128 - kRegsCtl) / 2 / 8 * 8;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -213,7 +219,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // MMA warpgroup needs few registers, the two softmax warpgroups hold a
     // whole S row (128 f32) each.
     if (warp == 0) {
-        setmaxnreg_dec<56>();
+        setmaxnreg_dec<kRegsCtl>();
         // ------------------------------------------------------------ producer
         uint32_t kc = 0, qc = 0;  // K/V tiles and query pairs loaded so far
         const int lanes = 32 / C;
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
     } else if (warp == 1) {
-        setmaxnreg_dec<56>();
+        setmaxnreg_dec<kRegsCtl>();
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t qa0 = smem_u32(S.q[0]), qb0 = smem_u32(S.q[1]);
@@ -390,9 +396,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         }
         __syncwarp();
     } else if (warp < 4) {
-        setmaxnreg_dec<56>();  // warps 2-3: no role, donate registers
+        setmaxnreg_dec<kRegsCtl>();  // warps 2-3: no role, donate registers
     } else {
-        setmaxnreg_inc<224>();
+        setmaxnreg_inc<kRegsSoftmax>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
         const int quad = warp & 3;
@@ -548,37 +554,95 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         static_cast<double>(l_sel) / static_cast<double>(l);
                 continue;
             }
-            // O_X to registers, then release TMEM to the next item's PV
-            uint32_t o[128];
+            // O_X chunk by chunk (32 columns), then release TMEM to the next
+            // item's first PV_X
             if (nX > 0) {
                 mbar_wait(&S.bar_o_done[X], (tc - 1) & 1);
                 tc_fence_after();
-                tmem_ld32(tO + 0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-                tmem_ld32(tO + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-                tmem_ld32(tO + 64, *reinterpret_cast<uint32_t(*)[32]>(&o[64]));
-                tmem_ld32(tO + 96, *reinterpret_cast<uint32_t(*)[32]>(&o[96]));
-                tmem_wait_ld();
-                tc_fence_before();
-                mbar_arrive(&S.bar_o_empty[X]);
-            } else {
-#pragma unroll
-                for (int jj = 0; jj < 128; ++jj) o[jj] = 0u;
             }
             const bool valid_row = row < P.n;
             const size_t rowoff = (static_cast<size_t>(I.h) * P.n + (valid_row ? row : 0)) * kD;
+            float fo = 1.f, fa = 0.f, inv = 1.f;  // O scale, anchor-state scale, 1/l
             if (MODE == ANCHOR) {
-                const float mt2 = m_raw * c;
-                const float f = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
+                fo = (m_used == -INFINITY) ? 0.f : ex2(m_used - m_raw * c);
+            } else if (MODE == SPARSE) {
+                const float ma = valid_row ? P.m_in[static_cast<size_t>(I.h) * P.n + row] : 0.f;
+                const float la = valid_row ? P.l_in[static_cast<size_t>(I.h) * P.n + row] : 1.f;
+                const float ma2 = ma * kLog2e;
+                const float M = fmaxf(ma2, m_used);
+                fa = ex2(ma2 - M);
+                fo = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
+                inv = 1.f / (la * fa + l * fo);
+            } else {
+                inv = 1.f / l;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t o[32];
+                if (nX > 0) {
+                    tmem_ld32(tO + ch * 32, o);
+                    tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) o[jj] = 0u;
+                }
+                if (valid_row) {
+                    float w[32];
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) w[jj] = __uint_as_float(o[jj]) * fo;
+                    if (MODE == ANCHOR) {
+                        float* acc = P.acc_out + rowoff + ch * 32;
+#pragma unroll
+                        for (int jj = 0; jj < 32; jj += 4)
+                            *reinterpret_cast<float4*>(acc + jj) =
+                                make_float4(w[jj], w[jj + 1], w[jj + 2], w[jj + 3]);
+                    } else {
+                        if (MODE == SPARSE) {
+                            const float* acc_a = P.acc_in + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 4) {
+                                const float4 a = *reinterpret_cast<const float4*>(acc_a + jj);
+                                w[jj] += a.x * fa;
+                                w[jj + 1] += a.y * fa;
+                                w[jj + 2] += a.z * fa;
+                                w[jj + 3] += a.w * fa;
+                            }
+                        }
+                        if (P.out_bf16) {
+                            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(P.out) + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 8) {
+                                uint4 u;
+                                __nv_bfloat162 t0 = __floats2bfloat162_rn(w[jj] * inv, w[jj + 1] * inv);
+                                __nv_bfloat162 t1 = __floats2bfloat162_rn(w[jj + 2] * inv, w[jj + 3] * inv);
+                                __nv_bfloat162 t2 = __floats2bfloat162_rn(w[jj + 4] * inv, w[jj + 5] * inv);
+                                __nv_bfloat162 t3 = __floats2bfloat162_rn(w[jj + 6] * inv, w[jj + 7] * inv);
+                                u.x = *reinterpret_cast<uint32_t*>(&t0);
+                                u.y = *reinterpret_cast<uint32_t*>(&t1);
+                                u.z = *reinterpret_cast<uint32_t*>(&t2);
+                                u.w = *reinterpret_cast<uint32_t*>(&t3);
+                                *reinterpret_cast<uint4*>(out + jj) = u;
+                            }
+                        } else {
+                            float* out = static_cast<float*>(P.out) + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 4)
+                                *reinterpret_cast<float4*>(out + jj) = make_float4(
+                                    w[jj] * inv, w[jj + 1] * inv, w[jj + 2] * inv, w[jj + 3] * inv);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (nX > 0) {
+                tc_fence_before();
+                mbar_arrive(&S.bar_o_empty[X]);
+            }
+            if (MODE == ANCHOR) {
                 const float m_nat = m_raw * P.inv_sqrt_d;
                 if (valid_row) {
-                    float* acc = P.acc_out + rowoff;
-#pragma unroll
-                    for (int jj = 0; jj < kD; jj += 4)
-                        *reinterpret_cast<float4*>(acc + jj) = make_float4(
-                            __uint_as_float(o[jj]) * f, __uint_as_float(o[jj + 1]) * f,
-                            __uint_as_float(o[jj + 2]) * f, __uint_as_float(o[jj + 3]) * f);
                     P.m_out[static_cast<size_t>(I.h) * P.n + row] = m_nat;
-                    P.l_out[static_cast<size_t>(I.h) * P.n + row] = l * f;
+                    P.l_out[static_cast<size_t>(I.h) * P.n + row] = l * fo;
                 }
                 if (P.msum != nullptr) {
                     float ms = valid_row ? m_nat : 0.f;
@@ -593,62 +657,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
                     else asm volatile("bar.sync 2, 128;" ::: "memory");
                 }
-            } else if (valid_row) {
-                float fa = 0.f, fs = 1.f, inv = 0.f;
-                if (MODE == SPARSE) {
-                    const float ma = P.m_in[static_cast<size_t>(I.h) * P.n + row];
-                    const float la = P.l_in[static_cast<size_t>(I.h) * P.n + row];
-                    const float ma2 = ma * kLog2e;
-                    const float M = fmaxf(ma2, m_used);
-                    fa = ex2(ma2 - M);
-                    fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
-                    inv = 1.f / (la * fa + l * fs);
-                } else {
-                    inv = 1.f / l;
-                }
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    float w[32];
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) w[jj] = __uint_as_float(o[ch * 32 + jj]) * fs;
-                    if (MODE == SPARSE) {
-                        const float* acc_a = P.acc_in + rowoff + ch * 32;
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 4) {
-                            const float4 a = *reinterpret_cast<const float4*>(acc_a + jj);
-                            w[jj] += a.x * fa;
-                            w[jj + 1] += a.y * fa;
-                            w[jj + 2] += a.z * fa;
-                            w[jj + 3] += a.w * fa;
-                        }
-                    }
-                    if (P.out_bf16) {
-                        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(P.out) + rowoff + ch * 32;
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 8) {
-                            uint4 u;
-                            __nv_bfloat162 t0 = __floats2bfloat162_rn(w[jj] * inv, w[jj + 1] * inv);
-                            __nv_bfloat162 t1 = __floats2bfloat162_rn(w[jj + 2] * inv, w[jj + 3] * inv);
-                            __nv_bfloat162 t2 = __floats2bfloat162_rn(w[jj + 4] * inv, w[jj + 5] * inv);
-                            __nv_bfloat162 t3 = __floats2bfloat162_rn(w[jj + 6] * inv, w[jj + 7] * inv);
-                            u.x = *reinterpret_cast<uint32_t*>(&t0);
-                            u.y = *reinterpret_cast<uint32_t*>(&t1);
-                            u.z = *reinterpret_cast<uint32_t*>(&t2);
-                            u.w = *reinterpret_cast<uint32_t*>(&t3);
-                            *reinterpret_cast<uint4*>(out + jj) = u;
-                        }
-                    } else {
-                        float* out = static_cast<float*>(P.out) + rowoff + ch * 32;
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 4)
-                            *reinterpret_cast<float4*>(out + jj) = make_float4(
-                                w[jj] * inv, w[jj + 1] * inv, w[jj + 2] * inv, w[jj + 3] * inv);
-                    }
-                }
             }
         }
     }
-
     tc_fence_before();
     if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
