@@ -37,12 +37,18 @@ constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
 constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
-// fa_pair register split per warpgroup (setmaxnreg; 128*ctl + 256*softmax <= 64K)
+// fa_pair register split per warpgroup (setmaxnreg).  The CTA launches with
+// 168 registers per thread (384 threads); the softmax warpgroups can only grow
+// by what the control warpgroup gives back: 256*(soft - 168) <= 128*(168 - ctl)
+// (a larger increase blocks setmaxnreg.inc forever).
 #ifndef AA_REGS_CTL
 #define AA_REGS_CTL 88
 #endif
+constexpr uint32_t kRegsLaunch = 168;
 constexpr uint32_t kRegsCtl = AA_REGS_CTL;
-constexpr uint32_t kRegsSoftmax = (65536 / 128 - kRegsCtl) / 2 / 8 * 8;
+constexpr uint32_t kRegsSoftmax = (kRegsLaunch + (kRegsLaunch - kRegsCtl) / 2) / 8 * 8;
+static_assert(256 * (kRegsSoftmax - kRegsLaunch) <= 128 * (kRegsLaunch - kRegsCtl),
+              "setmaxnreg.inc would wait for registers that are never released");
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
