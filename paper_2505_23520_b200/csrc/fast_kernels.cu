@@ -1046,8 +1046,19 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int items = P.groups * ipg * f.hq / P.cluster;
+    // One item per CTA: the hardware block scheduler is the load balancer.
+    // Measured (128k Llama, profiles/README.md): a static persistent stride
+    // over the heavy-first list was 1.7x slower for K3 (4-CTA clusters: only
+    // 132 of 148 SMs can hold one, so the last clusters run afterwards) and
+    // 11% slower for K1 (the stride aliases with the pair index).  The kernel
+    // keeps the multi-item loop (q_empty / o_empty hand-over) for AA_PERSISTENT.
+#ifdef AA_PERSISTENT
     const unsigned grid =
         static_cast<unsigned>(std::min(items, std::max(1, sms / P.cluster)) * P.cluster);
+#else
+    (void)sms;
+    const unsigned grid = static_cast<unsigned>(items * P.cluster);
+#endif
     if (P.cluster == 1) {
         fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
         return cudaGetLastError();
