@@ -37,18 +37,6 @@ constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
 constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
-// fa_pair register split per warpgroup (setmaxnreg).  The CTA launches with
-// 168 registers per thread (384 threads); the softmax warpgroups can only grow
-// by what the control warpgroup gives back: 256*(soft - 168) <= 128*(168 - ctl)
-// (a larger increase blocks setmaxnreg.inc forever).
-#ifndef AA_REGS_CTL
-#define AA_REGS_CTL 88
-#endif
-constexpr uint32_t kRegsLaunch = 168;
-constexpr uint32_t kRegsCtl = AA_REGS_CTL;
-constexpr uint32_t kRegsSoftmax = (kRegsLaunch + (kRegsLaunch - kRegsCtl) / 2) / 8 * 8;
-static_assert(256 * (kRegsSoftmax - kRegsLaunch) <= 128 * (kRegsLaunch - kRegsCtl),
-              "setmaxnreg.inc would wait for registers that are never released");
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -104,9 +92,9 @@ struct PairSmem {
     uint8_t q[2][kTileBytes];
     uint8_t k[2][kTileBytes];
     uint8_t v[2][kTileBytes];
-    uint64_t bar_q, bar_q_empty;
+    uint64_t bar_q;
     uint64_t bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
-    uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2], bar_o_empty[2];  // per query tile
+    uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
     float red[2][4];
 };
@@ -116,66 +104,19 @@ __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
     return it == 0 ? 0 : wsb + it - 1;  // ANCHOR: {0} then [wsb, qb]
 }
 
-// One work item = two query blocks (A = qb, B = qb + 1) of one head and one
-// group.  Items are numbered heavy-first (last groups first); within a group
-// the pairs of one head are adjacent, then the heads of one KV head, so CTAs
-// running together gather the same stripe rows (GQA siblings select mostly
-// the same keys) and the gathers hit L2.
-struct Item {
-    int gi, h, kvh, qA, qB, nA, nB, ntiles, wsb, count;
-    bool valid, hasB;
-    const uint32_t* list;
-};
-
-template <int MODE>
-__device__ __forceinline__ Item decode_item(const FaParams& P, int L) {
-    Item it{};
-    const int ipg = (P.step + 1) / 2;  // query-block pairs per group
-    it.gi = P.groups - 1 - L / (ipg * P.hq);
-    const int rem = L % (ipg * P.hq);
-    it.h = rem / ipg;
-    const int pi = ipg - 1 - rem % ipg;
-    it.kvh = it.h / P.rep;
-    it.qA = it.gi * P.step + 2 * pi;
-    it.qB = it.qA + 1;
-    it.valid = it.qA < P.T_m;
-    it.hasB = it.valid && (2 * pi + 1 < P.step) && (it.qB < P.T_m);
-    if (!it.valid) return it;
-    if (MODE == DENSE || MODE == RECALL) {
-        it.nA = it.qA + 1;
-        it.nB = it.hasB ? it.qB + 1 : 0;
-    } else if (MODE == ANCHOR) {
-        const int rb = it.gi * P.step * kB;
-        it.wsb = rb < 2 * kB ? 1 : rb / kB - 1;
-        it.nA = 1 + (it.qA >= it.wsb ? it.qA - it.wsb + 1 : 0);
-        it.nB = it.hasB ? 1 + (it.qB - it.wsb + 1) : 0;
-    } else {
-        it.count = P.counts[it.h * P.groups + it.gi];
-        it.list = P.csr ? P.idx + P.offsets[it.h * P.groups + it.gi]
-                        : P.idx + it.h * P.cap + P.offsets[it.gi];
-        it.nA = (it.count + kB - 1) / kB;
-        it.nB = it.hasB ? it.nA : 0;
-    }
-    it.ntiles = it.nA > it.nB ? it.nA : it.nB;
-    return it;
-}
-
-// Persistent FA-style tile engine, one CTA per SM; 12 warps:
-//   warp 0      TMA producer (Q pair per item; K and V through 2-stage rings,
-//               gather4 for K3), running ahead into the next item
+// One CTA = two query blocks (A = qb, B = qb + 1) of one head and one group;
+// they share every K/V tile (and for K3 the same gathered stripe rows), so
+// each tile is loaded once for 256 query rows.  12 warps:
+//   warp 0      TMA producer (Q pair once; K and V through 2-stage rings)
 //   warp 1      TMEM allocator (512 columns) + single-thread MMA issuer
 //   warps 4-7   softmax / epilogue of query tile A   (TMEM lanes 0..127)
 //   warps 8-11  softmax / epilogue of query tile B
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512); P_X is written
 // as f16 over S_X columns [0,64) and consumed from TMEM by O_X += P_X V.
 // MMA order per tile j:  PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1) — the tensor
-// pipe works on one query tile's MMAs while the other tile's softmax runs
-// (FA4-style ping-pong); tcgen05 MMAs of one thread execute in issue order, so
-// QK_X(j+1) overwriting S_X after PV_X(j) has read P_X is ordered by the pipe.
-// Across items: the next item's Q load waits only for the last QK of the
-// current one (bar_q_empty), its first PV_X for the epilogue's read of O_X
-// (bar_o_empty), so loads and QKs of item i+1 overlap the epilogue of item i.
-// All ring / barrier phases are running counters over the CTA's item list.
+// pipe works on one tile's MMAs while the other tile's softmax runs (FA4-style
+// ping-pong); tcgen05 MMAs of one thread execute in issue order, so QK_X(j+1)
+// overwriting S_X after PV_X(j) has read P_X is ordered by the pipe.
 template <int MODE>
 __global__ void __launch_bounds__(kPairThreads, 1)
     fa_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -187,23 +128,50 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // K3 cluster mode (P.cluster = C > 1): the C CTAs of a cluster take the C
-    // pairs of one (head, group) item block and so walk the same gathered
-    // tiles; each CTA gathers 128/C rows of every tile and multicasts them, and
+    // work item: heavy-first (last groups first).  Within a group, the pairs of
+    // one head are adjacent, then the heads of one KV head: CTAs that run
+    // together gather the same stripe rows (one list per (head, group); GQA
+    // siblings select mostly the same keys), so the gathers hit L2.
+    const int ipg = (P.step + 1) / 2;  // query-block pairs per group
+    const int L = blockIdx.x;
+    const int gi = P.groups - 1 - L / (ipg * P.hq);
+    const int rem = L % (ipg * P.hq);
+    const int h = rem / ipg;
+    const int pi = ipg - 1 - rem % ipg;
+    const int kvh = h / P.rep;
+    const int qA = gi * P.step + 2 * pi;
+    if (qA >= P.T_m) return;
+    const bool hasB = (2 * pi + 1 < P.step) && (qA + 1 < P.T_m);
+    const int qB = qA + 1;
+
+    int nA = 0, nB = 0, wsb = 0, count = 0;
+    const uint32_t* list = nullptr;
+    if (MODE == DENSE || MODE == RECALL) {
+        nA = qA + 1;
+        nB = hasB ? qB + 1 : 0;
+    } else if (MODE == ANCHOR) {
+        const int rb = gi * P.step * kB;
+        wsb = rb < 2 * kB ? 1 : rb / kB - 1;
+        nA = 1 + (qA >= wsb ? qA - wsb + 1 : 0);
+        nB = hasB ? 1 + (qB - wsb + 1) : 0;
+    } else {
+        count = P.counts[h * P.groups + gi];
+        list = P.csr ? P.idx + P.offsets[h * P.groups + gi] : P.idx + h * P.cap + P.offsets[gi];
+        nA = (count + kB - 1) / kB;
+        nB = hasB ? nA : 0;
+    }
+    const int ntiles = nA > nB ? nA : nB;
+
+    // K3 cluster mode (P.cluster = C > 1): the C CTAs of a cluster are C pairs
+    // of the same (head, group) and so walk the same gathered tiles; each CTA
+    // gathers 128/C rows of every tile and multicasts them to all C CTAs, and
     // a K/V stage is refilled only after all C consumers released it.
     const int C = MODE == SPARSE ? P.cluster : 1;
     const uint32_t crank = C > 1 ? cluster_ctarank() : 0;
     const uint16_t cmask = static_cast<uint16_t>((1u << C) - 1u);
-    const int ipg = (P.step + 1) / 2;
-    const int n_cluster_items = P.groups * ipg * P.hq / C;
-    const int cid = blockIdx.x / C, ncl = gridDim.x / C;
-    // query-block buffer release: the MMA's last QK (+ the softmax threads'
-    // reads of Q for the pooled partial sums in ANCHOR mode)
-    const uint32_t q_release = MODE == ANCHOR ? 1 + 2 * 128 : 1;
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
-        mbar_init(&S.bar_q_empty, q_release);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&S.bar_k_full[b], 1);
             mbar_init(&S.bar_k_empty[b], C);
@@ -212,7 +180,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             mbar_init(&S.bar_s_full[b], 1);
             mbar_init(&S.bar_p_full[b], 128);
             mbar_init(&S.bar_o_done[b], 1);
-            mbar_init(&S.bar_o_empty[b], 128);
         }
         fence_mbar_init();
     }
@@ -225,245 +192,201 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // MMA warpgroup needs few registers, the two softmax warpgroups hold a
     // whole S row (128 f32) each.
     if (warp == 0) {
-        setmaxnreg_dec<kRegsCtl>();
+        setmaxnreg_dec<56>();
         // ------------------------------------------------------------ producer
-        uint32_t kc = 0, qc = 0;  // K/V tiles and query pairs loaded so far
-        const int lanes = 32 / C;
-        const bool gl = lane < lanes;
-        const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
-        for (int ci = cid; ci < n_cluster_items; ci += ncl) {
-            const Item I = decode_item<MODE>(P, ci * C + static_cast<int>(crank));
-            if (!I.valid || I.ntiles == 0) continue;
-            if (lane == 0) {
-                if (qc > 0) mbar_wait(&S.bar_q_empty, (qc - 1) & 1);
-                mbar_expect_tx(&S.bar_q, I.hasB ? 2 * kTileBytes : kTileBytes);
-                tma_load_3d(S.q[0], &tmQ, &S.bar_q, 0, I.qA * kB, I.h);
-                tma_load_3d(S.q[0] + kAtomBytes, &tmQ, &S.bar_q, 64, I.qA * kB, I.h);
-                if (I.hasB) {
-                    tma_load_3d(S.q[1], &tmQ, &S.bar_q, 0, I.qB * kB, I.h);
-                    tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, I.qB * kB, I.h);
-                }
+        if (lane == 0 && ntiles > 0) {
+            mbar_expect_tx(&S.bar_q, hasB ? 2 * kTileBytes : kTileBytes);
+            tma_load_3d(S.q[0], &tmQ, &S.bar_q, 0, qA * kB, h);
+            tma_load_3d(S.q[0] + kAtomBytes, &tmQ, &S.bar_q, 64, qA * kB, h);
+            if (hasB) {
+                tma_load_3d(S.q[1], &tmQ, &S.bar_q, 0, qB * kB, h);
+                tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
             }
-            ++qc;
-            if (MODE == SPARSE) {
-                // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
-                // column halves, for K and for V).  Standalone CTA: 32 lanes
-                // cover the 128 rows; in a cluster of C, this CTA covers rows
-                // [crank*128/C, (crank+1)*128/C) and multicasts them.
-                auto fetch = [&](int t, int (&j)[4]) {
-                    const int base = t * kB;
+        }
+        if (MODE == SPARSE) {
+            // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
+            // column halves, for K and for V).  Standalone CTA: 32 lanes cover
+            // the 128 rows; in a cluster of C, this CTA covers rows
+            // [crank*128/C, (crank+1)*128/C) and multicasts them.
+            const int lanes = 32 / C;
+            const bool gl = lane < lanes;
+            const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
+            auto fetch = [&](int t, int (&j)[4]) {
+                const int base = t * kB;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = base + row0 + u;
-                        j[u] = gl ? static_cast<int>(I.list[e < I.count ? e : base]) : 0;
-                    }
-                };
-                int j[4];
-                fetch(0, j);
-                const int vh = I.kvh * P.n;  // V16 scratch is packed [hkv, n, d]
-                for (int it = 0; it < I.ntiles; ++it, ++kc) {
-                    const int st = kc & 1;
-                    int rk[4];
+                for (int u = 0; u < 4; ++u) {
+                    const int e = base + row0 + u;
+                    j[u] = gl ? static_cast<int>(list[e < count ? e : base]) : 0;
+                }
+            };
+            int j[4];
+            if (ntiles > 0) fetch(0, j);
+            const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
+            for (int it = 0; it < ntiles; ++it) {
+                const int st = it & 1;
+                int rk[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) rk[u] = I.kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
-                    if (lane == 0) {
-                        if (kc >= 2) mbar_wait(&S.bar_k_empty[st], ((kc >> 1) - 1) & 1);
-                        mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
+                for (int u = 0; u < 4; ++u) rk[u] = kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
+                if (lane == 0) {
+                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
+                }
+                __syncwarp();
+                uint8_t* kd = S.k[st] + row0 * 128;
+                if (gl) {
+                    if (C > 1) {
+                        tma_gather4_mc(kd, &tmKg, &S.bar_k_full[st], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], cmask, 64, rk[0], rk[1],
+                                       rk[2], rk[3]);
+                    } else {
+                        tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1], rk[2],
+                                    rk[3]);
                     }
-                    __syncwarp();
-                    uint8_t* kd = S.k[st] + row0 * 128;
-                    if (gl) {
-                        if (C > 1) {
-                            tma_gather4_mc(kd, &tmKg, &S.bar_k_full[st], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
-                            tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], cmask, 64, rk[0],
-                                           rk[1], rk[2], rk[3]);
-                        } else {
-                            tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
-                            tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1],
-                                        rk[2], rk[3]);
-                        }
+                }
+                if (lane == 0) {
+                    if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
+                }
+                __syncwarp();
+                uint8_t* vd = S.v[st] + row0 * 128;
+                if (gl) {
+                    if (C > 1) {
+                        tma_gather4_mc(vd, &tmVg, &S.bar_v_full[st], cmask, 0, vh + j[0], vh + j[1],
+                                       vh + j[2], vh + j[3]);
+                        tma_gather4_mc(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], cmask, 64, vh + j[0],
+                                       vh + j[1], vh + j[2], vh + j[3]);
+                    } else {
+                        tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1], vh + j[2],
+                                    vh + j[3]);
+                        tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0], vh + j[1],
+                                    vh + j[2], vh + j[3]);
                     }
-                    if (lane == 0) {
-                        if (kc >= 2) mbar_wait(&S.bar_v_empty[st], ((kc >> 1) - 1) & 1);
+                }
+                if (it + 1 < ntiles) fetch(it + 1, j);
+            }
+        } else {
+            for (int it = 0; it < ntiles; ++it) {
+                if (lane == 0) {
+                    const int st = it & 1;
+                    const int kt = kv_tile_of(MODE, it, wsb);
+                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
+                    tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
+                    tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
+                    if (MODE != RECALL) {
+                        if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                         mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
+                        tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
+                        tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
                     }
-                    __syncwarp();
-                    uint8_t* vd = S.v[st] + row0 * 128;
-                    if (gl) {
-                        if (C > 1) {
-                            tma_gather4_mc(vd, &tmVg, &S.bar_v_full[st], cmask, 0, vh + j[0], vh + j[1],
-                                           vh + j[2], vh + j[3]);
-                            tma_gather4_mc(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], cmask, 64,
-                                           vh + j[0], vh + j[1], vh + j[2], vh + j[3]);
-                        } else {
-                            tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1],
-                                        vh + j[2], vh + j[3]);
-                            tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0],
-                                        vh + j[1], vh + j[2], vh + j[3]);
-                        }
-                    }
-                    if (it + 1 < I.ntiles) fetch(it + 1, j);
                 }
-            } else {
-                for (int it = 0; it < I.ntiles; ++it, ++kc) {
-                    if (lane == 0) {
-                        const int st = kc & 1;
-                        const int kt = kv_tile_of(MODE, it, I.wsb);
-                        if (kc >= 2) mbar_wait(&S.bar_k_empty[st], ((kc >> 1) - 1) & 1);
-                        mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
-                        tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, I.kvh);
-                        tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, I.kvh);
-                        if (MODE != RECALL) {
-                            if (kc >= 2) mbar_wait(&S.bar_v_empty[st], ((kc >> 1) - 1) & 1);
-                            mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
-                            tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, I.kvh);
-                            tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB,
-                                        I.kvh);
-                        }
-                    }
-                    __syncwarp();
-                }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
-        setmaxnreg_dec<kRegsCtl>();
+        setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        if (lane == 0 && ntiles > 0) {
             const uint32_t qa0 = smem_u32(S.q[0]), qb0 = smem_u32(S.q[1]);
-            uint32_t kc = 0, qc = 0;     // tiles / query pairs consumed
-            uint32_t tcX[2] = {0, 0};    // tiles per query tile (S/P/O barrier phases)
-            uint32_t ocX[2] = {0, 0};    // items whose O_X an epilogue must release
+            auto qk = [&](int X, int j) {
+                const int st = j & 1;
+                mbar_wait(&S.bar_k_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t q0 = X ? qb0 : qa0, k0 = smem_u32(S.k[st]);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+                    mma_ss(tmem + X * 128, sdesc_sw128(q0 + off, 16, 1024),
+                           sdesc_sw128(k0 + off, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&S.bar_s_full[X]);
+            };
+            auto pv = [&](int X, int j) {
+                const int st = j & 1;
+                mbar_wait(&S.bar_p_full[X], j & 1);
+                if (MODE == RECALL) return;  // S_X(j) consumed; no PV
+                mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t v0 = smem_u32(S.v[st]);
+                const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ts(tO, tS + kk * 8, sdesc_sw128(v0 + kk * 2048, kAtomBytes, 1024), kIdescPV,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+                mma_commit(&S.bar_o_done[X]);
+            };
             // a stage is released to every producer of the cluster that fills it
             auto release = [&](uint64_t* bar) {
                 if (C > 1) mma_commit_mc(bar, cmask); else mma_commit(bar);
             };
-            for (int ci = cid; ci < n_cluster_items; ci += ncl) {
-                const Item I = decode_item<MODE>(P, ci * C + static_cast<int>(crank));
-                if (!I.valid || I.ntiles == 0) continue;
-                const int nX[2] = {I.nA, I.nB};
-                auto qk = [&](int X, int j) {
-                    const uint32_t k = kc + j, st = k & 1;
-                    mbar_wait(&S.bar_k_full[st], (k >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t q0 = X ? qb0 : qa0, k0 = smem_u32(S.k[st]);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-                        mma_ss(tmem + X * 128, sdesc_sw128(q0 + off, 16, 1024),
-                               sdesc_sw128(k0 + off, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
-                    }
-                    mma_commit(&S.bar_s_full[X]);
-                };
-                auto pv = [&](int X, int j) {
-                    const uint32_t k = kc + j, st = k & 1;
-                    mbar_wait(&S.bar_p_full[X], (tcX[X] + j) & 1);
-                    if (MODE == RECALL) return;  // S_X(j) consumed; no PV
-                    if (j == 0 && ocX[X] > 0) mbar_wait(&S.bar_o_empty[X], (ocX[X] - 1) & 1);
-                    mbar_wait(&S.bar_v_full[st], (k >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t v0 = smem_u32(S.v[st]);
-                    const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        mma_ts(tO, tS + kk * 8, sdesc_sw128(v0 + kk * 2048, kAtomBytes, 1024), kIdescPV,
-                               (j > 0 || kk > 0) ? 1u : 0u);
-                    mma_commit(&S.bar_o_done[X]);
-                };
-                mbar_wait(&S.bar_q, qc & 1);
-                if (I.nA > 0) qk(0, 0);
-                if (I.nB > 0) qk(1, 0);
-                release(&S.bar_k_empty[kc & 1]);
-                if (I.ntiles == 1) mma_commit(&S.bar_q_empty);
-                for (int j = 0; j < I.ntiles; ++j) {
-                    for (int X = 0; X < 2; ++X) {
-                        if (j < nX[X]) {
-                            pv(X, j);
-                            if (j + 1 < nX[X]) qk(X, j + 1);
-                        }
-                    }
-                    if (j + 2 == I.ntiles) mma_commit(&S.bar_q_empty);  // last QK issued
-                    release(&S.bar_v_empty[(kc + j) & 1]);
-                    if (j + 1 < I.ntiles) release(&S.bar_k_empty[(kc + j + 1) & 1]);
+            mbar_wait(&S.bar_q, 0);
+            if (nA > 0) qk(0, 0);
+            if (nB > 0) qk(1, 0);
+            release(&S.bar_k_empty[0]);
+            for (int j = 0; j < ntiles; ++j) {
+                if (j < nA) {
+                    pv(0, j);
+                    if (j + 1 < nA) qk(0, j + 1);
                 }
-                kc += I.ntiles;
-                ++qc;
-                for (int X = 0; X < 2; ++X) {
-                    tcX[X] += nX[X];
-                    if (nX[X] > 0 && MODE != RECALL) ++ocX[X];
+                if (j < nB) {
+                    pv(1, j);
+                    if (j + 1 < nB) qk(1, j + 1);
                 }
+                release(&S.bar_v_empty[j & 1]);
+                if (j + 1 < ntiles) release(&S.bar_k_empty[(j + 1) & 1]);
             }
-            if (C > 1 && kc > 0) {
+            if (C > 1) {
                 // every CTA's last releases have landed here before the exit
                 // cluster barrier, so no remote arrive can target a retired CTA
-                const uint32_t jl = kc - 1;
+                const int jl = ntiles - 1;
                 mbar_wait(&S.bar_k_empty[jl & 1], (jl >> 1) & 1);
                 mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
             }
         }
         __syncwarp();
     } else if (warp < 4) {
-        setmaxnreg_dec<kRegsCtl>();  // warps 2-3: no role, donate registers
+        setmaxnreg_dec<56>();  // warps 2-3: no role, donate registers
     } else {
-        setmaxnreg_inc<kRegsSoftmax>();
+        setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
-        const int quad = warp & 3;
-        const int r = quad * 32 + lane;
-        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t tS = tmem + X * 128 + lane_off;
-        const uint32_t tO = tmem + 256 + X * 128 + lane_off;
-        const float c = P.scale_log2;
-        uint32_t tc = 0, qc = 0;  // tiles of this query tile / query pairs seen
-        for (int ci = cid; ci < n_cluster_items; ci += ncl) {
-            const Item I = decode_item<MODE>(P, ci * C + static_cast<int>(crank));
-            if (!I.valid) continue;
-            const int nX = X ? I.nB : I.nA;
-            const int qx = X ? I.qB : I.qA;
-            const bool active = X == 0 || I.hasB;  // this query tile exists
+        const int nX = X ? nB : nA;
+        const int qx = X ? qB : qA;
+        if (X == 1 && !hasB) {
+            // no second query block in this item
+        } else {
+            const int quad = warp & 3;
+            const int r = quad * 32 + lane;
             const int row = qx * kB + r;
-            if (MODE == ANCHOR && I.ntiles > 0) {
-                // pooled-query partials: column r of this query tile summed over
-                // its 128 rows (zero past n), then release the Q buffer
-                mbar_wait(&S.bar_q, qc & 1);
-                if (active && P.qsum != nullptr) {
-                    const uint8_t* atom = S.q[X] + (r >> 6) * kAtomBytes;
-                    const int chunk = (r & 63) >> 3, e = r & 7;
-                    float s = 0.f;
-                    for (int rr = 0; rr < kB; ++rr) {
-                        const __nv_bfloat16 x = *reinterpret_cast<const __nv_bfloat16*>(
-                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4) + e * 2);
-                        s += __bfloat162float(x);
-                    }
-                    P.qsum[(static_cast<size_t>(I.h) * P.T_m + qx) * kD + r] = s;
-                }
-                mbar_arrive(&S.bar_q_empty);
-            }
-            if (I.ntiles > 0) ++qc;
-            if (!active) continue;
-
+            const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+            const uint32_t tS = tmem + X * 128 + lane_off;
+            const uint32_t tO = tmem + 256 + X * 128 + lane_off;
+            const float c = P.scale_log2;
             float m_used = -INFINITY;  // running max, log2 units (lazy)
             float m_raw = -INFINITY;   // true max of raw q.k
             float l = 0.f;
             float l_sel = 0.f;         // RECALL: mass of the selected keys
+            // RECALL: this row group's stripe bitmask row and window start
             const uint32_t* bits_x = nullptr;
             int wstart_x = 0;
             if (MODE == RECALL) {
-                bits_x = P.bits + (static_cast<int64_t>(I.h) * P.groups + I.gi) * P.words_per_row;
-                const int rb = I.gi * P.step * kB;
+                bits_x = P.bits + (static_cast<int64_t>(h) * P.groups + gi) * P.words_per_row;
+                const int rb = gi * P.step * kB;
                 const int wsbx = rb < 2 * kB ? 1 : rb / kB - 1;
                 wstart_x = min(wsbx * kB, P.n);
             }
 
-            for (int it = 0; it < nX; ++it, ++tc) {
+            for (int it = 0; it < nX; ++it) {
                 int lim;
                 if (MODE == SPARSE) {
-                    lim = min(kB, I.count - it * kB);
+                    lim = min(kB, count - it * kB);
                 } else {
-                    const int kt = kv_tile_of(MODE, it, I.wsb);
+                    const int kt = kv_tile_of(MODE, it, wsb);
                     lim = min(kB, P.n - kt * kB);
                     if (kt == qx) lim = min(lim, r + 1);
                 }
-                mbar_wait(&S.bar_s_full[X], tc & 1);
+                mbar_wait(&S.bar_s_full[X], it & 1);
                 tc_fence_after();
                 // single pass: the whole S row in registers
                 uint32_t v[128];
@@ -477,7 +400,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     for (int jj = 0; jj < kB; ++jj)
                         if (jj >= lim) v[jj] = 0xff800000u;  // -inf -> p = 0
                 }
-                const float mx = row_max128(v);
+                float mx = row_max128(v);
                 m_raw = fmaxf(m_raw, mx);
                 const float mx2 = mx * c;
                 bool rescale = false;
@@ -494,9 +417,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     // block and the local window are covered; middle keys are
                     // selected iff their stripe bit is set
                     l_sel *= alpha;
+                    const int kt = it;
                     uint32_t sel[4] = {~0u, ~0u, ~0u, ~0u};
-                    if (it > 0 && it * kB < wstart_x) {
-                        const uint4 w = *reinterpret_cast<const uint4*>(bits_x + 4 * (it - 1));
+                    if (kt > 0 && kt * kB < wstart_x) {
+                        const uint4 w = *reinterpret_cast<const uint4*>(bits_x + 4 * (kt - 1));
                         sel[0] = w.x, sel[1] = w.y, sel[2] = w.z, sel[3] = w.w;
                     }
                     float2 la = make_float2(0.f, 0.f), ls = make_float2(0.f, 0.f);
@@ -526,6 +450,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
                                                            __uint_as_float(v[ch * 32 + jj + 1])),
                                                c, -base);
+                        // 12 of every 32 exponentials on the FMA pipe, the rest on
+                        // MUFU: balances the two pipes (MUFU alone needs as many
+                        // cycles per tile as the tensor core)
                         const float2 pp = (jj >> 1) % 16 < kPolyPairs
                                               ? ex2_poly2(x)
                                               : make_float2(ex2(x.x), ex2(x.y));
@@ -539,13 +466,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     if (!rescale) alpha = 1.f;
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) {
-                        uint32_t o[32];
-                        tmem_ld32(tO + ch * 32, o);
+                        uint32_t v[32];
+                        tmem_ld32(tO + ch * 32, v);
                         tmem_wait_ld();
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
-                            o[jj] = __float_as_uint(__uint_as_float(o[jj]) * alpha);
-                        tmem_st32(tO + ch * 32, o);
+                            v[jj] = __float_as_uint(__uint_as_float(v[jj]) * alpha);
+                        tmem_st32(tO + ch * 32, v);
                     }
                 }
                 tmem_wait_st();
@@ -553,119 +480,135 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_arrive(&S.bar_p_full[X]);
             }
 
-            // ------------------------------------------------------------ epilogue
+            // -------------------------------------------------------- epilogue
             if (MODE == RECALL) {
                 if (row < P.n)
-                    P.row_recall[static_cast<size_t>(I.h) * P.n + row] =
+                    P.row_recall[static_cast<size_t>(h) * P.n + row] =
                         static_cast<double>(l_sel) / static_cast<double>(l);
-                continue;
-            }
-            // O_X chunk by chunk (32 columns), then release TMEM to the next
-            // item's first PV_X
+            } else {
             if (nX > 0) {
-                mbar_wait(&S.bar_o_done[X], (tc - 1) & 1);
+                mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
                 tc_fence_after();
             }
             const bool valid_row = row < P.n;
-            const size_t rowoff = (static_cast<size_t>(I.h) * P.n + (valid_row ? row : 0)) * kD;
-            float fo = 1.f, fa = 0.f, inv = 1.f;  // O scale, anchor-state scale, 1/l
+            const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
             if (MODE == ANCHOR) {
-                fo = (m_used == -INFINITY) ? 0.f : ex2(m_used - m_raw * c);
-            } else if (MODE == SPARSE) {
-                const float ma = valid_row ? P.m_in[static_cast<size_t>(I.h) * P.n + row] : 0.f;
-                const float la = valid_row ? P.l_in[static_cast<size_t>(I.h) * P.n + row] : 1.f;
-                const float ma2 = ma * kLog2e;
-                const float M = fmaxf(ma2, m_used);
-                fa = ex2(ma2 - M);
-                fo = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
-                inv = 1.f / (la * fa + l * fo);
-            } else {
-                inv = 1.f / l;
-            }
+                const float mt2 = m_raw * c;
+                const float f = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
+                float* acc = P.acc_out + rowoff;
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t o[32];
-                if (nX > 0) {
-                    tmem_ld32(tO + ch * 32, o);
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tO + ch * 32, v);
                     tmem_wait_ld();
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) o[jj] = 0u;
-                }
-                if (valid_row) {
-                    float w[32];
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) w[jj] = __uint_as_float(o[jj]) * fo;
-                    if (MODE == ANCHOR) {
-                        float* acc = P.acc_out + rowoff + ch * 32;
+                    if (valid_row) {
 #pragma unroll
                         for (int jj = 0; jj < 32; jj += 4)
-                            *reinterpret_cast<float4*>(acc + jj) =
-                                make_float4(w[jj], w[jj + 1], w[jj + 2], w[jj + 3]);
+                            *reinterpret_cast<float4*>(acc + ch * 32 + jj) = make_float4(
+                                __uint_as_float(v[jj]) * f, __uint_as_float(v[jj + 1]) * f,
+                                __uint_as_float(v[jj + 2]) * f, __uint_as_float(v[jj + 3]) * f);
+                    }
+                    __syncwarp();
+                }
+                const float m_nat = m_raw * P.inv_sqrt_d;
+                if (valid_row) {
+                    P.m_out[static_cast<size_t>(h) * P.n + row] = m_nat;
+                    P.l_out[static_cast<size_t>(h) * P.n + row] = l * f;
+                }
+                if (P.msum != nullptr) {
+                    float ms = valid_row ? m_nat : 0.f;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
+                    if (lane == 0) S.red[X][quad] = ms;
+                }
+                if (P.qsum != nullptr) {
+                    // column r of this query tile, summed over its 128 rows (zero past n)
+                    const int col = r;
+                    const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes;
+                    const int chunk = (col & 63) >> 3, e = col & 7;
+                    float s = 0.f;
+                    for (int rr = 0; rr < kB; ++rr) {
+                        const __nv_bfloat16 x = *reinterpret_cast<const __nv_bfloat16*>(
+                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4) + e * 2);
+                        s += __bfloat162float(x);
+                    }
+                    P.qsum[(static_cast<size_t>(h) * P.T_m + qx) * kD + col] = s;
+                }
+                if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+                else asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (P.msum != nullptr && quad == 0 && lane == 0) {
+                    P.msum[static_cast<size_t>(h) * P.T_m + qx] =
+                        static_cast<double>(S.red[X][0]) + S.red[X][1] + S.red[X][2] + S.red[X][3];
+                }
+            } else {
+                float fa = 0.f, fs = 1.f, inv = 0.f;
+                const float* acc_a = nullptr;
+                if (MODE == SPARSE) {
+                    const float ma = valid_row ? P.m_in[static_cast<size_t>(h) * P.n + row] : 0.f;
+                    const float la = valid_row ? P.l_in[static_cast<size_t>(h) * P.n + row] : 1.f;
+                    const float ma2 = ma * kLog2e;
+                    const float M = fmaxf(ma2, m_used);
+                    fa = ex2(ma2 - M);
+                    fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
+                    inv = 1.f / (la * fa + l * fs);
+                    acc_a = P.acc_in + rowoff;
+                } else {
+                    inv = 1.f / l;
+                }
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    if (nX > 0) {
+                        tmem_ld32(tO + ch * 32, v);
+                        tmem_wait_ld();
                     } else {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) v[jj] = 0u;
+                    }
+                    if (valid_row) {
+                        float o[32];
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) o[jj] = __uint_as_float(v[jj]) * fs;
                         if (MODE == SPARSE) {
-                            const float* acc_a = P.acc_in + rowoff + ch * 32;
 #pragma unroll
                             for (int jj = 0; jj < 32; jj += 4) {
-                                const float4 a = *reinterpret_cast<const float4*>(acc_a + jj);
-                                w[jj] += a.x * fa;
-                                w[jj + 1] += a.y * fa;
-                                w[jj + 2] += a.z * fa;
-                                w[jj + 3] += a.w * fa;
+                                const float4 a = *reinterpret_cast<const float4*>(acc_a + ch * 32 + jj);
+                                o[jj] += a.x * fa;
+                                o[jj + 1] += a.y * fa;
+                                o[jj + 2] += a.z * fa;
+                                o[jj + 3] += a.w * fa;
                             }
                         }
                         if (P.out_bf16) {
                             __nv_bfloat16* out = static_cast<__nv_bfloat16*>(P.out) + rowoff + ch * 32;
 #pragma unroll
                             for (int jj = 0; jj < 32; jj += 8) {
-                                uint4 u;
-                                __nv_bfloat162 t0 = __floats2bfloat162_rn(w[jj] * inv, w[jj + 1] * inv);
-                                __nv_bfloat162 t1 = __floats2bfloat162_rn(w[jj + 2] * inv, w[jj + 3] * inv);
-                                __nv_bfloat162 t2 = __floats2bfloat162_rn(w[jj + 4] * inv, w[jj + 5] * inv);
-                                __nv_bfloat162 t3 = __floats2bfloat162_rn(w[jj + 6] * inv, w[jj + 7] * inv);
-                                u.x = *reinterpret_cast<uint32_t*>(&t0);
-                                u.y = *reinterpret_cast<uint32_t*>(&t1);
-                                u.z = *reinterpret_cast<uint32_t*>(&t2);
-                                u.w = *reinterpret_cast<uint32_t*>(&t3);
-                                *reinterpret_cast<uint4*>(out + jj) = u;
+                                uint4 w;
+                                __nv_bfloat162 t0 = __floats2bfloat162_rn(o[jj] * inv, o[jj + 1] * inv);
+                                __nv_bfloat162 t1 = __floats2bfloat162_rn(o[jj + 2] * inv, o[jj + 3] * inv);
+                                __nv_bfloat162 t2 = __floats2bfloat162_rn(o[jj + 4] * inv, o[jj + 5] * inv);
+                                __nv_bfloat162 t3 = __floats2bfloat162_rn(o[jj + 6] * inv, o[jj + 7] * inv);
+                                w.x = *reinterpret_cast<uint32_t*>(&t0);
+                                w.y = *reinterpret_cast<uint32_t*>(&t1);
+                                w.z = *reinterpret_cast<uint32_t*>(&t2);
+                                w.w = *reinterpret_cast<uint32_t*>(&t3);
+                                *reinterpret_cast<uint4*>(out + jj) = w;
                             }
                         } else {
                             float* out = static_cast<float*>(P.out) + rowoff + ch * 32;
 #pragma unroll
                             for (int jj = 0; jj < 32; jj += 4)
                                 *reinterpret_cast<float4*>(out + jj) = make_float4(
-                                    w[jj] * inv, w[jj + 1] * inv, w[jj + 2] * inv, w[jj + 3] * inv);
+                                    o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
                         }
                     }
-                }
-                __syncwarp();
-            }
-            if (nX > 0) {
-                tc_fence_before();
-                mbar_arrive(&S.bar_o_empty[X]);
-            }
-            if (MODE == ANCHOR) {
-                const float m_nat = m_raw * P.inv_sqrt_d;
-                if (valid_row) {
-                    P.m_out[static_cast<size_t>(I.h) * P.n + row] = m_nat;
-                    P.l_out[static_cast<size_t>(I.h) * P.n + row] = l * fo;
-                }
-                if (P.msum != nullptr) {
-                    float ms = valid_row ? m_nat : 0.f;
-#pragma unroll
-                    for (int sh = 16; sh; sh >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, sh);
-                    if (lane == 0) S.red[X][quad] = ms;
-                    if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-                    else asm volatile("bar.sync 2, 128;" ::: "memory");
-                    if (quad == 0 && lane == 0)
-                        P.msum[static_cast<size_t>(I.h) * P.T_m + qx] =
-                            static_cast<double>(S.red[X][0]) + S.red[X][1] + S.red[X][2] + S.red[X][3];
-                    if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-                    else asm volatile("bar.sync 2, 128;" ::: "memory");
+                    __syncwarp();
                 }
             }
+            }  // MODE != RECALL
         }
     }
+
     tc_fence_before();
     if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
@@ -1026,9 +969,10 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
         attr_set[MODE] = true;
     }
     const int ipg = (P.step + 1) / 2;
+    const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
     // K3: cluster the pairs of one (head, group) so each gathered tile is
     // fetched once per cluster (TMA multicast); needs every group complete
-    // (no placeholder items) and the pairs of a group to fill whole clusters.
+    // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
     P.cluster = 1;
     if (MODE == SPARSE && P.T_m % P.step == 0) {
         for (int c : {4, 2})
@@ -1037,28 +981,6 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
                 break;
             }
     }
-    // persistent: one CTA per SM (a multiple of the cluster size), each walking
-    // the heavy-first item list with a stride of the grid
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int items = P.groups * ipg * f.hq / P.cluster;
-    // One item per CTA: the hardware block scheduler is the load balancer.
-    // Measured (128k Llama, profiles/README.md): a static persistent stride
-    // over the heavy-first list was 1.7x slower for K3 (4-CTA clusters: only
-    // 132 of 148 SMs can hold one, so the last clusters run afterwards) and
-    // 11% slower for K1 (the stride aliases with the pair index).  The kernel
-    // keeps the multi-item loop (q_empty / o_empty hand-over) for AA_PERSISTENT.
-#ifdef AA_PERSISTENT
-    const unsigned grid =
-        static_cast<unsigned>(std::min(items, std::max(1, sms / P.cluster)) * P.cluster);
-#else
-    (void)sms;
-    const unsigned grid = static_cast<unsigned>(items * P.cluster);
-#endif
     if (P.cluster == 1) {
         fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
         return cudaGetLastError();
