@@ -968,6 +968,9 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
             return e;
         attr_set[MODE] = true;
     }
+#ifndef AA_CLUSTER_MAX
+#define AA_CLUSTER_MAX 4
+#endif
     const int ipg = (P.step + 1) / 2;
     const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
     // K3: cluster the pairs of one (head, group) so each gathered tile is
@@ -975,7 +978,7 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
     P.cluster = 1;
     if (MODE == SPARSE && P.T_m % P.step == 0) {
-        for (int c : {4, 2})
+        for (int c : {AA_CLUSTER_MAX, 2})
             if (ipg % c == 0) {
                 P.cluster = c;
                 break;
