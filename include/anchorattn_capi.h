@@ -180,6 +180,14 @@ aa_status aa_union_recall(const aa_problem* p, const void* q, const void* k,
                           const uint32_t* indices, const int32_t* counts, double* recall,
                           aa_stream_t stream);
 
+/* Softmax mass of every (query block, key block) tile of dense causal
+ * attention: tile_mass [hq, ceil(n/b_q), ceil(n/b_kv)] f32, row-normalised
+ * probabilities summed over the tile (the block-granularity score map of
+ * R/src/baselines.cpp:62-83, pooled_score_map, computed without the n x n
+ * map).  Fast path only (AA_BF16). */
+aa_status aa_dense_tile_mass(const aa_problem* p, const void* q, const void* k,
+                             float* tile_mass, aa_stream_t stream);
+
 /* Stage timing for profilers/benchmarks: while set, the fast path of
  * aa_anchor_attention records events[i] (cudaEvent_t) on its stream at the
  * stage boundaries 0 start | 1 V->f16 | 2 K1 anchor | 3 pool + K2 identify +

@@ -82,6 +82,7 @@ def lib():
             "aa_union_recall": [P, p, p, p, p, p, p],
             "aa_stream_sync": [p],
             "aa_set_stage_events": [C.POINTER(C.c_void_p), C.c_int],
+            "aa_dense_tile_mass": [P, p, p, p, p],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -294,6 +295,16 @@ def union_recall(q, k, idx, counts, cfg=BlockConfig()):
     _check(lib().aa_union_recall(C.byref(p), _ptr(q), _ptr(k), _ptr(idx), _ptr(counts), _ptr(r),
                                  _stream()))
     return r
+
+
+def dense_tile_mass(q, k, cfg=BlockConfig()):
+    """Softmax mass per (query block, key block) tile, [hq, T_m, T_n] f32."""
+    p = make_problem(q, k, cfg)
+    hq, n, _ = q.shape
+    T = (n + 127) // 128
+    m = torch.zeros((hq, T, T), dtype=torch.float32, device=q.device)
+    _check(lib().aa_dense_tile_mass(C.byref(p), _ptr(q), _ptr(k), _ptr(m), _stream()))
+    return m
 
 
 def anchor_attention_host(q, k, v, cfg=BlockConfig(), zero_anchor=False,

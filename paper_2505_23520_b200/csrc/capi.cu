@@ -507,6 +507,18 @@ aa_status aa_set_stage_events(void* const* events, int count) {
     return AA_OK;
 }
 
+aa_status aa_dense_tile_mass(const aa_problem* p, const void* q, const void* k,
+                             float* tile_mass, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (p->dtype != AA_BF16)
+        return fail(AA_ERR_UNSUPPORTED, "aa_dense_tile_mass: bf16 (tcgen05) path only");
+    if (aa_status s = require_device()) return s;
+    AA_CUDA(aa::fast_tile_mass(fast_args(*p), q, k, tile_mass,
+                               reinterpret_cast<cudaStream_t>(stream)));
+    return AA_OK;
+}
+
 aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const void* k,
                                    const void* v, int zero_anchor, void* out, aa_dtype out_dtype,
                                    int64_t* computed) {

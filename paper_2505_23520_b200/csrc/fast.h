@@ -41,6 +41,11 @@ cudaError_t fast_finalize(const FastArgs& f, const float* l, const float* acc, v
 // D — dense causal FlashAttention-style tcgen05 kernel (the speed baseline).
 cudaError_t fast_dense(const FastArgs& f, const void* q, const void* k, const void* v16, void* out,
                        aa_dtype out_dtype, cudaStream_t s);
+// Exact softmax mass of every (query block, key block) tile of the dense
+// causal attention, [hq, T_m, T_n] f32 (two QK-only passes; for the
+// block-granularity comparison).
+cudaError_t fast_tile_mass(const FastArgs& f, const void* q, const void* k, float* tile_mass,
+                           cudaStream_t s);
 // Recall of the union mask from one dense pass.
 cudaError_t fast_recall(const FastArgs& f, const void* q, const void* k, const uint32_t* indices,
                         const int32_t* counts, const int64_t* offsets, int64_t cap,

@@ -53,7 +53,12 @@ constexpr int kPolyPairs = AA_POLY_PAIRS;
 
 // RECALL: the dense causal QK pass without PV, accumulating per row the
 // softmax mass of all keys and of the selected keys (covered ∪ stripes).
-enum Mode { ANCHOR = 0, SPARSE = 1, DENSE = 2, RECALL = 3 };
+// TILEMASS: a second QK-only pass that uses RECALL's per-row (max, sum) to
+// write the exact softmax mass of every (query block, key block) tile.
+enum Mode { ANCHOR = 0, SPARSE = 1, DENSE = 2, RECALL = 3, TILEMASS = 4 };
+
+template <int MODE>
+constexpr bool kQkOnly = MODE == RECALL || MODE == TILEMASS;
 
 struct FaParams {
     int n, hq, rep, T_m, step;
@@ -85,6 +90,9 @@ struct FaParams {
     const uint32_t* bits;   // selection bitmask [hq, G, words_per_row]
     int64_t words_per_row;
     double* row_recall;     // [hq, n]: selected / total softmax mass per row
+    float2* row_stats;      // [hq, n]: (running max in log2 units, sum) — RECALL out, TILEMASS in
+    float* tile_mass;       // [hq, T_m, T_n] TILEMASS output
+    int T_n;
 };
 
 // Shared memory of fa_pair: two query tiles, 2-stage K and V rings.
@@ -96,11 +104,11 @@ struct PairSmem {
     uint64_t bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
-    float red[2][4];
+    float red[2][2][4];
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
-    if (mode == DENSE || mode == RECALL) return it;
+    if (mode == DENSE || mode == RECALL || mode == TILEMASS) return it;
     return it == 0 ? 0 : wsb + it - 1;  // ANCHOR: {0} then [wsb, qb]
 }
 
@@ -146,7 +154,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
     int nA = 0, nB = 0, wsb = 0, count = 0;
     const uint32_t* list = nullptr;
-    if (MODE == DENSE || MODE == RECALL) {
+    if (MODE == DENSE || kQkOnly<MODE>) {
         nA = qA + 1;
         nB = hasB ? qB + 1 : 0;
     } else if (MODE == ANCHOR) {
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
                     tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
                     tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
-                    if (MODE != RECALL) {
+                    if (!kQkOnly<MODE>) {
                         if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                         mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
                         tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             auto pv = [&](int X, int j) {
                 const int st = j & 1;
                 mbar_wait(&S.bar_p_full[X], j & 1);
-                if (MODE == RECALL) return;  // S_X(j) consumed; no PV
+                if (kQkOnly<MODE>) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t v0 = smem_u32(S.v[st]);
@@ -400,6 +408,36 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     for (int jj = 0; jj < kB; ++jj)
                         if (jj >= lim) v[jj] = 0xff800000u;  // -inf -> p = 0
                 }
+                if constexpr (MODE == TILEMASS) {
+                    // exact normalised mass of this (query block, key tile):
+                    // per-row sum with RECALL's final (max, sum), reduced over
+                    // the 128 rows of the query tile
+                    float rm = 0.f;
+                    if (row < P.n) {
+                        const float2 st = P.row_stats[static_cast<size_t>(h) * P.n + row];
+                        float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int jj = 0; jj < kB; jj += 2) {
+                            const float2 x = ffma2(make_float2(__uint_as_float(v[jj]),
+                                                               __uint_as_float(v[jj + 1])),
+                                                   c, -st.x);
+                            acc2 = fadd2(acc2, make_float2(ex2(x.x), ex2(x.y)));
+                        }
+                        rm = (acc2.x + acc2.y) / st.y;
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&S.bar_p_full[X]);  // S consumed
+#pragma unroll
+                    for (int sh = 16; sh; sh >>= 1) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
+                    if (lane == 0) S.red[X][it & 1][quad] = rm;
+                    if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+                    else asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (quad == 0 && lane == 0)
+                        P.tile_mass[(static_cast<size_t>(h) * P.T_m + qx) * P.T_n + it] =
+                            S.red[X][it & 1][0] + S.red[X][it & 1][1] + S.red[X][it & 1][2] +
+                            S.red[X][it & 1][3];
+                    continue;
+                }
                 float mx = row_max128(v);
                 m_raw = fmaxf(m_raw, mx);
                 const float mx2 = mx * c;
@@ -481,10 +519,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
 
             // -------------------------------------------------------- epilogue
-            if (MODE == RECALL) {
-                if (row < P.n)
+            if (kQkOnly<MODE>) {
+                if (MODE == RECALL && row < P.n) {
                     P.row_recall[static_cast<size_t>(h) * P.n + row] =
                         static_cast<double>(l_sel) / static_cast<double>(l);
+                    if (P.row_stats)
+                        P.row_stats[static_cast<size_t>(h) * P.n + row] = make_float2(m_used, l);
+                }
             } else {
             if (nX > 0) {
                 mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
@@ -519,7 +560,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     float ms = valid_row ? m_nat : 0.f;
 #pragma unroll
                     for (int o = 16; o; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
-                    if (lane == 0) S.red[X][quad] = ms;
+                    if (lane == 0) S.red[X][0][quad] = ms;
                 }
                 if (P.qsum != nullptr) {
                     // column r of this query tile, summed over its 128 rows (zero past n)
@@ -538,7 +579,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 else asm volatile("bar.sync 2, 128;" ::: "memory");
                 if (P.msum != nullptr && quad == 0 && lane == 0) {
                     P.msum[static_cast<size_t>(h) * P.T_m + qx] =
-                        static_cast<double>(S.red[X][0]) + S.red[X][1] + S.red[X][2] + S.red[X][3];
+                        static_cast<double>(S.red[X][0][0]) + S.red[X][0][1] + S.red[X][0][2] + S.red[X][0][3];
                 }
             } else {
                 float fa = 0.f, fs = 1.f, inv = 0.f;
@@ -961,7 +1002,8 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     P.scale_log2 = kLog2e * P.inv_sqrt_d;
     P.kv_head_rows = static_cast<int>(f.kv_hs / kD);
     P.kv_row_rows = static_cast<int>(f.kv_rs / kD);
-    static bool attr_set[4] = {false, false, false, false};
+    P.T_n = static_cast<int>((n + kB - 1) / kB);
+    static bool attr_set[5] = {false, false, false, false, false};
     if (!attr_set[MODE]) {
         if ((e = cudaFuncSetAttribute(fa_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kSmemBytes))))
@@ -1142,6 +1184,38 @@ cudaError_t fast_recall(const FastArgs& f, const void* q, const void* k, const u
         e = cudaGetLastError();
     }
     cudaFreeAsync(bits, s);
+    return e;
+}
+
+cudaError_t fast_tile_mass(const FastArgs& f, const void* q, const void* k, float* tile_mass,
+                           cudaStream_t s) {
+    const int64_t G = f.geo.groups(), n = f.geo.n;
+    const int64_t wpr = ((n + 31) / 32 + 3) / 4 * 4;
+    const size_t bits_b = static_cast<size_t>(f.hq * G * wpr) * 4;
+    const size_t rec_b = static_cast<size_t>(f.hq * n) * 8;
+    const size_t st_b = static_cast<size_t>(f.hq * n) * 8;
+    char* tmp = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), bits_b + rec_b + st_b, s))) return e;
+    if ((e = cudaMemsetAsync(tmp, 0, bits_b, s))) {
+        cudaFreeAsync(tmp, s);
+        return e;
+    }
+    // pass 1: per-row (max, sum) of the dense causal softmax
+    FaParams P{};
+    P.bits = reinterpret_cast<const uint32_t*>(tmp);
+    P.words_per_row = wpr;
+    P.row_recall = reinterpret_cast<double*>(tmp + bits_b);
+    P.row_stats = reinterpret_cast<float2*>(tmp + bits_b + rec_b);
+    e = launch_fa<RECALL>(f, q, k, k, P, s);
+    if (e == cudaSuccess) {
+        // pass 2: normalised mass per (query block, key block) tile
+        FaParams P2{};
+        P2.row_stats = P.row_stats;
+        P2.tile_mass = tile_mass;
+        e = launch_fa<TILEMASS>(f, q, k, k, P2, s);
+    }
+    cudaFreeAsync(tmp, s);
     return e;
 }
 

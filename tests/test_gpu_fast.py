@@ -232,3 +232,25 @@ def test_recall_pass_matches_oracle(oracle, n, step, theta):
                                   idx[h].cpu().numpy().view(np.uint32),
                                   counts[h].cpu().numpy().astype(np.int64))
         assert abs(rec[h] - ref) <= 1e-4, (h, rec[h], ref)
+
+
+@pytest.mark.parametrize("n", [1024, 1100])
+def test_dense_tile_mass_matches_softmax(n):
+    """Two-pass TILEMASS map == tile sums of the f64 causal softmax (numpy)."""
+    c = capi()
+    q, k, v = gen(n, hq=2, hkv=1, seed=5 + n)
+    mass = c.dense_tile_mass(q.cuda(), k.cuda()).cpu().numpy()
+    T = (n + 127) // 128
+    for h in range(2):
+        qh = q[h].double().numpy()
+        kh = k[0].double().numpy()
+        s = qh @ kh.T / np.sqrt(128.0)
+        s[np.triu_indices(n, 1)] = -np.inf
+        p = np.exp(s - s.max(1, keepdims=True))
+        p /= p.sum(1, keepdims=True)
+        ref = np.zeros((T, T))
+        for a in range(T):
+            for b in range(T):
+                ref[a, b] = p[a * 128:(a + 1) * 128, b * 128:(b + 1) * 128].sum()
+        assert np.abs(mass[h] - ref).max() <= 2e-4
+        assert abs(mass[h].sum() - n) <= 1e-2 * n / 1000
