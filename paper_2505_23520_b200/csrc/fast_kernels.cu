@@ -438,19 +438,17 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                             S.red[X][it & 1][3];
                     continue;
                 }
-                float mx = row_max128(v);
-                m_raw = fmaxf(m_raw, mx);
-                const float mx2 = mx * c;
-                bool rescale = false;
-                float alpha = 1.f;
-                if (mx2 > m_used + 8.f) {
-                    alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx2);
-                    m_used = mx2;
-                    rescale = it > 0;
-                }
-                l *= alpha;
-                const float base = (m_used == -INFINITY) ? 0.f : m_used;
                 if constexpr (MODE == RECALL) {
+                    const float mx = row_max128(v);
+                    m_raw = fmaxf(m_raw, mx);
+                    const float mx2 = mx * c;
+                    float alpha = 1.f;
+                    if (mx2 > m_used + 8.f) {
+                        alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx2);
+                        m_used = mx2;
+                    }
+                    l *= alpha;
+                    const float base = (m_used == -INFINITY) ? 0.f : m_used;
                     // selected keys of this tile for this row's group: the initial
                     // block and the local window are covered; middle keys are
                     // selected iff their stripe bit is set
@@ -479,38 +477,60 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_arrive(&S.bar_p_full[X]);
                     continue;
                 }
-                float2 lsum = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int jj = 0; jj < 32; jj += 2) {
-                        const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
-                                                           __uint_as_float(v[ch * 32 + jj + 1])),
-                                               c, -base);
-                        // 12 of every 32 exponentials on the FMA pipe, the rest on
-                        // MUFU: balances the two pipes (MUFU alone needs as many
-                        // cycles per tile as the tensor core)
-                        const float2 pp = (jj >> 1) % 16 < kPolyPairs
-                                              ? ex2_poly2(x)
-                                              : make_float2(ex2(x.x), ex2(x.y));
-                        lsum = fadd2(lsum, pp);
-                        pk[jj >> 1] = pack_half2(pp.x, pp.y);
-                    }
-                    tmem_st16(tS + ch * 16, pk);
-                }
-                l += lsum.x + lsum.y;
-                if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective
-                    if (!rescale) alpha = 1.f;
+                // P = 2^(s*c - base) as f16 over S columns [0, 64); returns the row sum
+                auto emit = [&](float base) -> float {
+                    float2 lsum = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) {
-                        uint32_t v[32];
-                        tmem_ld32(tO + ch * 32, v);
-                        tmem_wait_ld();
+                        uint32_t pk[16];
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
-                            v[jj] = __float_as_uint(__uint_as_float(v[jj]) * alpha);
-                        tmem_st32(tO + ch * 32, v);
+                        for (int jj = 0; jj < 32; jj += 2) {
+                            const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
+                                                               __uint_as_float(v[ch * 32 + jj + 1])),
+                                                   c, -base);
+                            const float2 pp = (jj >> 1) % 16 < kPolyPairs
+                                                  ? ex2_poly2(x)
+                                                  : make_float2(ex2(x.x), ex2(x.y));
+                            lsum = fadd2(lsum, pp);
+                            pk[jj >> 1] = pack_half2(pp.x, pp.y);
+                        }
+                        tmem_st16(tS + ch * 16, pk);
+                    }
+                    return lsum.x + lsum.y;
+                };
+                if (it == 0) {
+                    // first tile: the row max sets the base
+                    const float mx = row_max128(v);
+                    m_raw = mx;
+                    m_used = mx * c;
+                    l = emit(m_used == -INFINITY ? 0.f : m_used);
+                } else {
+                    // Speculative: exponentials against the running (lazy) base
+                    // while the row max is reduced off the critical path; P values
+                    // up to 2^8 are fine in f16.  Only if the max grew by more than
+                    // 2^8 (rare) is the tile redone with the new base and O / l
+                    // rescaled.
+                    const float lsum = emit(m_used);
+                    const float mx = row_max128(v);
+                    m_raw = fmaxf(m_raw, mx);
+                    const float mx2 = mx * c;
+                    const bool redo = mx2 > m_used + 8.f;
+                    if (__any_sync(0xffffffffu, redo)) {  // tcgen05.ld/st are warp-collective
+                        const float alpha = redo ? ex2(m_used - mx2) : 1.f;
+                        if (redo) m_used = mx2;
+                        l = l * alpha + emit(m_used);
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + ch * 32, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj)
+                                o[jj] = __float_as_uint(__uint_as_float(o[jj]) * alpha);
+                            tmem_st32(tO + ch * 32, o);
+                        }
+                    } else {
+                        l += lsum;
                     }
                 }
                 tmem_wait_st();
