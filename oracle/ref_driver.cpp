@@ -21,6 +21,7 @@
 #include "anchorattn/parallel.hpp"
 #include "anchorattn/sparse_exec.hpp"
 #include "anchorattn/stripe_identify.hpp"
+#include "anchorattn/workload_io.hpp"
 #include "anchorattn/workloads.hpp"
 
 using namespace anchorattn;
@@ -193,5 +194,33 @@ int ref_gen_sink_local(std::int64_t n, std::int64_t d, double sink_strength,
 }
 
 std::int64_t ref_max_threads() { return static_cast<std::int64_t>(max_threads()); }
+
+// write_workload / read_workload (R/include/anchorattn/workload_io.hpp) for
+// byte-level checks of paper_2505_23520_b200.aqkv.  q/k/v: [heads, n, d].
+int ref_write_workload(const char* path, std::int64_t heads, std::int64_t n, std::int64_t d,
+                       const float* q, const float* k, const float* v) {
+    try {
+        std::vector<HeadWorkload> hs;
+        const std::size_t hd = static_cast<std::size_t>(n * d);
+        for (std::int64_t h = 0; h < heads; ++h)
+            hs.push_back(HeadWorkload::create(mat(q + h * hd, n, d), mat(k + h * hd, n, d),
+                                              mat(v + h * hd, n, d)));
+        write_workload(path, hs);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// Returns the number of heads read, or -1 with ref_last_error() set.
+std::int64_t ref_read_workload(const char* path) {
+    try {
+        return static_cast<std::int64_t>(read_workload(path).size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
 
 }  // extern "C"
