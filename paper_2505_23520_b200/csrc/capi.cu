@@ -5,6 +5,7 @@
 // no device is present.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -522,26 +523,56 @@ aa_status aa_dense_tile_mass(const aa_problem* p, const void* q, const void* k,
 aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const void* k,
                                    const void* v, int zero_anchor, void* out, aa_dtype out_dtype,
                                    int64_t* computed) {
+    // Pipelined over KV-head chunks (heads are independent, R/../SPEC.md:269):
+    // chunk c's inputs go up on the copy-in stream while chunk c-1 computes and
+    // chunk c-2's output comes back on the copy-out stream, so the PCIe
+    // transfers (both directions at once) hide the chain instead of adding to it.
     static std::mutex mu;
     static void* dbuf = nullptr;
     static size_t dbytes = 0;
-    static cudaStream_t st = nullptr;
+    static cudaStream_t st_in = nullptr, st_c = nullptr, st_out = nullptr;
+    constexpr int kMaxChunks = 8;
+    static cudaEvent_t ev_in[kMaxChunks], ev_done[kMaxChunks];
     std::lock_guard<std::mutex> lock(mu);
     aa_plan plan;
     if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (out_dtype != AA_F32 && out_dtype != AA_BF16)
+        return fail(AA_ERR_INVALID_ARGUMENT, "out_dtype must be AA_F32 or AA_BF16");
     const auto packed = [&](int64_t s, int64_t want) { return s == 0 || s == want; };
     if (!packed(p->q_row_stride, p->d) || !packed(p->q_head_stride, p->n * p->d) ||
         !packed(p->kv_row_stride, p->d) || !packed(p->kv_head_stride, p->n * p->d))
         return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_host: packed layouts only");
     if (aa_status s = require_device()) return s;
-    if (!st) AA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (!st_c) {
+        AA_CUDA(cudaStreamCreateWithFlags(&st_in, cudaStreamNonBlocking));
+        AA_CUDA(cudaStreamCreateWithFlags(&st_c, cudaStreamNonBlocking));
+        AA_CUDA(cudaStreamCreateWithFlags(&st_out, cudaStreamNonBlocking));
+        for (int c = 0; c < kMaxChunks; ++c) {
+            AA_CUDA(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
+            AA_CUDA(cudaEventCreateWithFlags(&ev_done[c], cudaEventDisableTiming));
+        }
+    }
+    const int64_t rep = p->hkv > 0 ? p->hq / p->hkv : 1;
+    const int64_t per = p->hkv > 0 ? (p->hkv + kMaxChunks - 1) / kMaxChunks : 1;  // KV heads per chunk
+    const int nchunks = p->hkv > 0 ? static_cast<int>((p->hkv + per - 1) / per) : 0;
+    aa_problem sub = *p;
+    sub.q_row_stride = sub.kv_row_stride = p->d;
+    sub.q_head_stride = sub.kv_head_stride = p->n * p->d;
+    sub.hkv = per;
+    sub.hq = per * rep;
+    aa_plan sub_plan;
+    if (nchunks > 0)
+        if (aa_status s = aa_make_plan(&sub, &sub_plan)) return s;
     const size_t es = p->dtype == AA_BF16 ? 2 : 4;
-    const size_t qb = static_cast<size_t>(p->hq * p->n * p->d) * es;
-    const size_t kvb = static_cast<size_t>(p->hkv * p->n * p->d) * es;
-    const size_t ob = static_cast<size_t>(p->hq * p->n * p->d) * (out_dtype == AA_BF16 ? 2 : 4);
+    const size_t os = out_dtype == AA_BF16 ? 2 : 4;
+    const size_t head_in = static_cast<size_t>(p->n * p->d) * es;
+    const size_t head_out = static_cast<size_t>(p->n * p->d) * os;
+    const size_t qb = static_cast<size_t>(p->hq) * head_in;
+    const size_t kvb = static_cast<size_t>(p->hkv) * head_in;
+    const size_t ob = static_cast<size_t>(p->hq) * head_out;
     const size_t cb = static_cast<size_t>(p->hq) * 8;
-    const size_t need = align256(qb) + 2 * align256(kvb) + align256(ob) + align256(cb) +
-                        plan.workspace_bytes;
+    const size_t ws_bytes = nchunks > 0 ? sub_plan.workspace_bytes : 0;
+    const size_t need = align256(qb) + 2 * align256(kvb) + align256(ob) + align256(cb) + ws_bytes;
     if (need > dbytes) {
         if (dbuf) AA_CUDA(cudaFree(dbuf));
         dbuf = nullptr;
@@ -550,21 +581,48 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
         dbytes = need;
     }
     char* b = static_cast<char*>(dbuf);
-    void* dq = b;
-    void* dk = b + align256(qb);
-    void* dv = static_cast<char*>(dk) + align256(kvb);
-    void* dout = static_cast<char*>(dv) + align256(kvb);
-    int64_t* dc = reinterpret_cast<int64_t*>(static_cast<char*>(dout) + align256(ob));
+    char* dq = b;
+    char* dk = dq + align256(qb);
+    char* dv = dk + align256(kvb);
+    char* dout = dv + align256(kvb);
+    int64_t* dc = reinterpret_cast<int64_t*>(dout + align256(ob));
     void* ws = reinterpret_cast<char*>(dc) + align256(cb);
-    AA_CUDA(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, st));
-    AA_CUDA(cudaMemcpyAsync(dk, k, kvb, cudaMemcpyHostToDevice, st));
-    AA_CUDA(cudaMemcpyAsync(dv, v, kvb, cudaMemcpyHostToDevice, st));
-    if (aa_status s = aa_anchor_attention(p, dq, dk, dv, zero_anchor, dout, out_dtype, dc, ws,
-                                          plan.workspace_bytes, reinterpret_cast<aa_stream_t>(st)))
-        return s;
-    AA_CUDA(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, st));
-    if (computed) AA_CUDA(cudaMemcpyAsync(computed, dc, cb, cudaMemcpyDeviceToHost, st));
-    AA_CUDA(cudaStreamSynchronize(st));
+    const char* hq_ = static_cast<const char*>(q);
+    const char* hk_ = static_cast<const char*>(k);
+    const char* hv_ = static_cast<const char*>(v);
+    char* ho_ = static_cast<char*>(out);
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t kv0 = c * per;
+        const int64_t nkv = std::min(per, p->hkv - kv0);
+        const int64_t h0 = kv0 * rep, nh = nkv * rep;
+        const size_t qo = static_cast<size_t>(h0) * head_in, qn = static_cast<size_t>(nh) * head_in;
+        const size_t ko = static_cast<size_t>(kv0) * head_in, kn = static_cast<size_t>(nkv) * head_in;
+        AA_CUDA(cudaMemcpyAsync(dq + qo, hq_ + qo, qn, cudaMemcpyHostToDevice, st_in));
+        AA_CUDA(cudaMemcpyAsync(dk + ko, hk_ + ko, kn, cudaMemcpyHostToDevice, st_in));
+        AA_CUDA(cudaMemcpyAsync(dv + ko, hv_ + ko, kn, cudaMemcpyHostToDevice, st_in));
+        AA_CUDA(cudaEventRecord(ev_in[c], st_in));
+        AA_CUDA(cudaStreamWaitEvent(st_c, ev_in[c], 0));
+        sub.hkv = nkv;
+        sub.hq = nh;
+        if (aa_status s = aa_anchor_attention(&sub, dq + qo, dk + ko, dv + ko, zero_anchor,
+                                              dout + static_cast<size_t>(h0) * head_out,
+                                              out_dtype, dc + h0, ws, ws_bytes,
+                                              reinterpret_cast<aa_stream_t>(st_c))) {
+            cudaStreamSynchronize(st_in);
+            cudaStreamSynchronize(st_c);
+            cudaStreamSynchronize(st_out);
+            return s;
+        }
+        AA_CUDA(cudaEventRecord(ev_done[c], st_c));
+        AA_CUDA(cudaStreamWaitEvent(st_out, ev_done[c], 0));
+        const size_t oo = static_cast<size_t>(h0) * head_out, on = static_cast<size_t>(nh) * head_out;
+        AA_CUDA(cudaMemcpyAsync(ho_ + oo, dout + oo, on, cudaMemcpyDeviceToHost, st_out));
+    }
+    if (computed && nchunks > 0)
+        AA_CUDA(cudaMemcpyAsync(computed, dc, cb, cudaMemcpyDeviceToHost, st_out));
+    AA_CUDA(cudaStreamSynchronize(st_in));
+    AA_CUDA(cudaStreamSynchronize(st_c));
+    AA_CUDA(cudaStreamSynchronize(st_out));
     return AA_OK;
 }
 

@@ -22,6 +22,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 #include <mutex>
 
 #include "fast.h"
@@ -86,6 +88,7 @@ struct FaParams {
     void* out;
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
+    int item0;    // first work item of this launch (K3 split launches)
     // RECALL inputs / output
     const uint32_t* bits;   // selection bitmask [hq, G, words_per_row]
     int64_t words_per_row;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // together gather the same stripe rows (one list per (head, group); GQA
     // siblings select mostly the same keys), so the gathers hit L2.
     const int ipg = (P.step + 1) / 2;  // query-block pairs per group
-    const int L = blockIdx.x;
+    const int L = blockIdx.x + P.item0;
     const int gi = P.groups - 1 - L / (ipg * P.hq);
     const int rem = L % (ipg * P.hq);
     const int h = rem / ipg;
@@ -1050,19 +1053,46 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
         fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
         return cudaGetLastError();
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kPairThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(P.cluster);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fa_pair<MODE>, tq, tk, tv, tkg, tvg, P);
+    auto launch_cluster = [&](const FaParams& PP, unsigned g, cudaStream_t st) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(g);
+        cfg.blockDim = dim3(kPairThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(PP.cluster);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fa_pair<MODE>, tq, tk, tv, tkg, tvg, PP);
+    };
+    // Clusters of 4 tile only part of the GPU's SMs (GPC sizes are not all
+    // multiples of 4); the lightest groups can go to a concurrent launch with
+    // clusters of 2 that runs on the SMs the first launch cannot use.
+    int split_groups = 0;
+    if (MODE == SPARSE && P.cluster == 4 && ipg % 2 == 0) {
+        if (const char* env = getenv("AA_K3_SPLIT_GROUPS")) split_groups = atoi(env);
+        split_groups = std::max(0, std::min(split_groups, P.groups - 1));
+    }
+    if (split_groups == 0) return launch_cluster(P, grid, s);
+    const unsigned grid2 = static_cast<unsigned>(split_groups * ipg * f.hq);
+    static cudaStream_t side = nullptr;
+    if (!side && (e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking))) return e;
+    cudaEvent_t fork, join;
+    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming))) return e;
+    FaParams P2 = P;
+    P2.item0 = static_cast<int>(grid - grid2);
+    P2.cluster = 2;
+    if (!(e = cudaEventRecord(fork, s)) && !(e = cudaStreamWaitEvent(side, fork, 0)) &&
+        !(e = launch_cluster(P, grid - grid2, s)) && !(e = launch_cluster(P2, grid2, side)) &&
+        !(e = cudaEventRecord(join, side)))
+        e = cudaStreamWaitEvent(s, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    return e;
 }
 
 cudaError_t convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s) {

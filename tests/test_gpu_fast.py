@@ -254,3 +254,24 @@ def test_dense_tile_mass_matches_softmax(n):
                 ref[a, b] = p[a * 128:(a + 1) * 128, b * 128:(b + 1) * 128].sum()
         assert np.abs(mass[h] - ref).max() <= 2e-4
         assert abs(mass[h].sum() - n) <= 1e-2 * n / 1000
+
+
+@pytest.mark.parametrize("hq,hkv,pinned", [(8, 2, True), (36, 12, True), (4, 4, False)])
+def test_host_entry_pipelined_equals_device_chain(hq, hkv, pinned):
+    """aa_anchor_attention_host (KV-head chunks pipelined over three streams)
+    returns exactly the device chain's output and per-head computed counts —
+    including head counts that do not split evenly into chunks and pageable
+    host buffers."""
+    c = capi()
+    n = 2048
+    q, k, v = gen(n, hq=hq, hkv=hkv, seed=hq + hkv)
+    cfg = c.BlockConfig()
+    ref, comp = c.anchor_attention(q.cuda(), k.cuda(), v.cuda(), cfg)
+    torch.cuda.synchronize()
+    if pinned:
+        q, k, v = q.pin_memory(), k.pin_memory(), v.pin_memory()
+    out, comp_h = c.anchor_attention_host(q, k, v, cfg)
+    assert torch.equal(out, ref.cpu())
+    assert torch.equal(comp_h, comp.cpu())
+    out16, _ = c.anchor_attention_host(q, k, v, cfg, out_dtype=torch.bfloat16)
+    assert torch.equal(out16.float(), ref.cpu().bfloat16().float())
