@@ -39,6 +39,7 @@ constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
 constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
+constexpr int kLsuThreads = 64;     // K3 lsu mode: warps 2-3 gather the stripe rows
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -52,6 +53,18 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define AA_POLY_PAIRS 0
 #endif
 constexpr int kPolyPairs = AA_POLY_PAIRS;
+
+// Optional cycle accounting of the fa_pair roles (build with -DAA_PROF; read
+// through aa_prof_read).  Slots: 0/1 softmax-A wait-S / compute, 2 softmax-A
+// tiles, 3/4/5 MMA wait P / K / V, 6 CTA cycles, 7 epilogue (softmax A),
+// 8 prologue (to the first S), 9 CTAs, 10 producer wait-empty, 11/12
+// softmax-B wait-S / compute.
+#ifdef AA_PROF
+__device__ unsigned long long g_prof[16];
+#define PROF(...) __VA_ARGS__
+#else
+#define PROF(...)
+#endif
 
 // RECALL: the dense causal QK pass without PV, accumulating per row the
 // softmax mass of all keys and of the selected keys (covered ∪ stripes).
@@ -89,6 +102,9 @@ struct FaParams {
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
     int item0;    // first work item of this launch (K3 split launches)
+    int lsu;      // K3: gather the stripe rows with cp.async (warps 2-3) instead of TMA gather4
+    const uint8_t* k_rows;    // K base (rows of d bf16, 256 B) for the LSU gathers
+    const uint8_t* v16_rows;  // packed f16 V [hkv, n, d]
     // RECALL inputs / output
     const uint32_t* bits;   // selection bitmask [hq, G, words_per_row]
     int64_t words_per_row;
@@ -103,7 +119,7 @@ struct PairSmem {
     uint8_t q[2][kTileBytes];
     uint8_t k[2][kTileBytes];
     uint8_t v[2][kTileBytes];
-    uint64_t bar_q;
+    uint64_t bar_q, bar_qsum;
     uint64_t bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
@@ -138,6 +154,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                                                ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    PROF(const long long t_cta0 = clock64();)
 
     // work item: heavy-first (last groups first).  Within a group, the pairs of
     // one head are adjacent, then the heads of one KV head: CTAs that run
@@ -183,10 +200,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
+        mbar_init(&S.bar_qsum, 64);
+        const uint32_t fills = (MODE == SPARSE && P.lsu) ? kLsuThreads : 1;
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&S.bar_k_full[b], 1);
+            mbar_init(&S.bar_k_full[b], fills);
             mbar_init(&S.bar_k_empty[b], C);
-            mbar_init(&S.bar_v_full[b], 1);
+            mbar_init(&S.bar_v_full[b], fills);
             mbar_init(&S.bar_v_empty[b], C);
             mbar_init(&S.bar_s_full[b], 1);
             mbar_init(&S.bar_p_full[b], 128);
@@ -214,7 +233,16 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
             }
         }
-        if (MODE == SPARSE) {
+        if (MODE == SPARSE && lane == 0 && ntiles > 0) {
+            // the epilogue's K1 state rows (acc: 64 KB per query tile) -> L2 now
+            for (int X = 0; X < (hasB ? 2 : 1); ++X) {
+                const int r0 = (X ? qB : qA) * kB;
+                const int rows = min(kB, P.n - r0);
+                bulk_prefetch_l2(P.acc_in + (static_cast<size_t>(h) * P.n + r0) * kD,
+                                 static_cast<uint32_t>(rows) * kD * 4);
+            }
+        }
+        if (MODE == SPARSE && !P.lsu) {
             // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
             // column halves, for K and for V).  Standalone CTA: 32 lanes cover
             // the 128 rows; in a cluster of C, this CTA covers rows
@@ -276,12 +304,14 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 if (it + 1 < ntiles) fetch(it + 1, j);
             }
-        } else {
+        } else if (MODE != SPARSE) {
             for (int it = 0; it < ntiles; ++it) {
                 if (lane == 0) {
                     const int st = it & 1;
                     const int kt = kv_tile_of(MODE, it, wsb);
+                    PROF(const long long t0 = clock64();)
                     if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    PROF(atomicAdd(&g_prof[10], clock64() - t0);)
                     mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
                     tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
                     tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
@@ -299,31 +329,47 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0 && ntiles > 0) {
-            const uint32_t qa0 = smem_u32(S.q[0]), qb0 = smem_u32(S.q[1]);
+            // SW128 descriptors: the high word (SBO 1024, version, layout) is a
+            // constant, the low word = start address >> 4 | LBO >> 4 << 16
+            constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
+            const uint32_t lq0 = sdesc_sw128_lo(smem_u32(S.q[0]), 16);
+            const uint32_t lq1 = sdesc_sw128_lo(smem_u32(S.q[1]), 16);
+            const uint32_t lk0 = sdesc_sw128_lo(smem_u32(S.k[0]), 16);
+            const uint32_t lv0 = sdesc_sw128_lo(smem_u32(S.v[0]), kAtomBytes);
+            PROF(long long pw_p = 0, pw_k = 0, pw_v = 0;)
             auto qk = [&](int X, int j) {
                 const int st = j & 1;
+                PROF(const long long t0 = clock64();)
                 mbar_wait(&S.bar_k_full[st], (j >> 1) & 1);
+                PROF(pw_k += clock64() - t0;)
                 tc_fence_after();
-                const uint32_t q0 = X ? qb0 : qa0, k0 = smem_u32(S.k[st]);
+                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
+                // descriptors are built once; the k-step only moves the start
+                // address field (addr >> 4, no carry below 256 KB)
+                const uint32_t lq = X ? lq1 : lq0, lk = lk0 + st * (kTileBytes >> 4);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-                    mma_ss(tmem + X * 128, sdesc_sw128(q0 + off, 16, 1024),
-                           sdesc_sw128(k0 + off, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+                    const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
+                    mma_ss(tmem + X * 128, kDescHi | (lq + off), kDescHi | (lk + off), kIdescQK,
+                           kk > 0 ? 1u : 0u);
                 }
                 mma_commit(&S.bar_s_full[X]);
             };
             auto pv = [&](int X, int j) {
                 const int st = j & 1;
+                PROF(const long long t0 = clock64();)
                 mbar_wait(&S.bar_p_full[X], j & 1);
+                PROF(const long long t1 = clock64(); pw_p += t1 - t0;)
                 if (kQkOnly<MODE>) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
+                PROF(pw_v += clock64() - t1;)
                 tc_fence_after();
-                const uint32_t v0 = smem_u32(S.v[st]);
+                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
+                const uint32_t lv = lv0 + st * (kTileBytes >> 4);
                 const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tO, tS + kk * 8, sdesc_sw128(v0 + kk * 2048, kAtomBytes, 1024), kIdescPV,
+                    mma_ts(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
                            (j > 0 || kk > 0) ? 1u : 0u);
                 mma_commit(&S.bar_o_done[X]);
             };
@@ -354,10 +400,97 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_k_empty[jl & 1], (jl >> 1) & 1);
                 mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
             }
+            PROF(atomicAdd(&g_prof[3], pw_p); atomicAdd(&g_prof[4], pw_k); atomicAdd(&g_prof[5], pw_v);)
         }
         __syncwarp();
     } else if (warp < 4) {
-        setmaxnreg_dec<56>();  // warps 2-3: no role, donate registers
+        setmaxnreg_dec<56>();  // warps 2-3: LSU gathers of K3 (lsu mode), K1 column sums
+        if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
+            // pooled-query partials (avgpool_rows, R/src/matrix.cpp:44-65): column
+            // sums of each query tile over its 128 rows (TMA zero-fills rows past
+            // n), summed in row order; thread t owns columns 2t, 2t+1.  Runs
+            // beside the main loop, off the epilogue's critical path.
+            const int t = threadIdx.x - 64;
+            const int col = 2 * t;
+            const int chunk = (col & 63) >> 3, e = col & 7;
+            mbar_wait(&S.bar_q, 0);
+            for (int X = 0; X < (hasB ? 2 : 1); ++X) {
+                const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes + e * 2;
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll 16
+                for (int rr = 0; rr < kB; ++rr) {
+                    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(
+                        atom + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+                    s0 += __low2float(x);
+                    s1 += __high2float(x);
+                }
+                *reinterpret_cast<float2*>(P.qsum + (static_cast<size_t>(h) * P.T_m + (X ? qB : qA)) * kD + col) =
+                    make_float2(s0, s1);
+            }
+            mbar_arrive(&S.bar_qsum);  // the epilogue reuses the Q tiles as staging
+        }
+        if (MODE == SPARSE && P.lsu) {
+            // Warp w in {2, 3} fills rows [64 (w - 2), 64 (w - 2) + 64) of every K
+            // and V tile; half-warp h copies row 2i + h, 16 lanes x 16 B = one
+            // 256-B row, into the 128B-swizzled K-major atoms TMA would write.
+            // Each thread waits for its own copies, fences them into the async
+            // proxy and arrives (full barriers count kLsuThreads arrivals).
+            const int wr = (warp - 2) * 64;
+            const int hsel = lane >> 4, sub = lane & 15;
+            const uint32_t chunk_off = static_cast<uint32_t>((sub >> 3) * kAtomBytes);
+            const int c8 = sub & 7;
+            const uint8_t* kbase = P.k_rows + static_cast<size_t>(kvh) * P.kv_head_rows * 256 + sub * 16;
+            const uint8_t* vbase = P.v16_rows + static_cast<size_t>(kvh) * P.n * 256 + sub * 16;
+            const size_t kstride = static_cast<size_t>(P.kv_row_rows) * 256;
+            for (int it = 0; it < ntiles; ++it) {
+                const int st = it & 1;
+                const int base = it * kB;
+                const int e0 = base + wr + lane, e1 = e0 + 32;
+                const uint32_t a0 = list[e0 < count ? e0 : base];
+                const uint32_t a1 = list[e1 < count ? e1 : base];
+                if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                const uint32_t kd = smem_u32(S.k[st]) + chunk_off;
+#pragma unroll 8
+                for (int i = 0; i < 32; ++i) {
+                    const int rho = 2 * i + hsel;  // row within this warp's 64
+                    const uint32_t j = __shfl_sync(0xffffffffu, i < 16 ? a0 : a1, rho & 31);
+                    const int r = wr + rho;
+                    cp_async16(kd + r * 128 + ((c8 ^ (r & 7)) << 4), kbase + j * kstride);
+                }
+                if (P.lsu == 2) {
+                    cp_async_arrive_noinc(&S.bar_k_full[st]);
+                } else {
+                    cp_async_commit();
+                    if (it >= 1) {  // V(it-1) landed
+                        cp_async_wait<1>();
+                        fence_proxy_async_smem();
+                        mbar_arrive(&S.bar_v_full[(it - 1) & 1]);
+                    }
+                }
+                if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                const uint32_t vd = smem_u32(S.v[st]) + chunk_off;
+#pragma unroll 8
+                for (int i = 0; i < 32; ++i) {
+                    const int rho = 2 * i + hsel;
+                    const uint32_t j = __shfl_sync(0xffffffffu, i < 16 ? a0 : a1, rho & 31);
+                    const int r = wr + rho;
+                    cp_async16(vd + r * 128 + ((c8 ^ (r & 7)) << 4), vbase + static_cast<size_t>(j) * 256);
+                }
+                if (P.lsu == 2) {
+                    cp_async_arrive_noinc(&S.bar_v_full[st]);
+                } else {
+                    cp_async_commit();
+                    cp_async_wait<1>();  // K(it) landed
+                    fence_proxy_async_smem();
+                    mbar_arrive(&S.bar_k_full[st]);
+                }
+            }
+            if (ntiles > 0 && P.lsu == 1) {
+                cp_async_wait<0>();
+                fence_proxy_async_smem();
+                mbar_arrive(&S.bar_v_full[(ntiles - 1) & 1]);
+            }
+        }
     } else {
         setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
@@ -388,6 +521,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 wstart_x = min(wsbx * kB, P.n);
             }
 
+            PROF(long long ps_wait = 0, ps_comp = 0, ps_t1 = 0, ps_first = 0;)
             for (int it = 0; it < nX; ++it) {
                 int lim;
                 if (MODE == SPARSE) {
@@ -397,20 +531,48 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     lim = min(kB, P.n - kt * kB);
                     if (kt == qx) lim = min(lim, r + 1);
                 }
+                PROF(const long long ps_t0 = clock64();)
                 mbar_wait(&S.bar_s_full[X], it & 1);
+                PROF(ps_t1 = clock64(); ps_wait += ps_t1 - ps_t0; if (it == 0) ps_first = ps_t1;)
                 tc_fence_after();
                 // single pass: the whole S row in registers
                 uint32_t v[128];
+                // P = 2^(s*c - base) as f16 over S columns [16 ch, 16 ch + 16)
+                // for S columns [32 ch, 32 ch + 32); accumulates the row sum
+                auto emit_chunk = [&](int ch, float base, float2& lsum) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int jj = 0; jj < 32; jj += 2) {
+                        const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
+                                                           __uint_as_float(v[ch * 32 + jj + 1])),
+                                               c, -base);
+                        const float2 pp = (jj >> 1) % 16 < kPolyPairs ? ex2_poly2(x)
+                                                                      : make_float2(ex2(x.x), ex2(x.y));
+                        lsum = fadd2(lsum, pp);
+                        pk[jj >> 1] = pack_half2(pp.x, pp.y);
+                    }
+                    tmem_st16(tS + ch * 16, pk);
+                };
+                auto emit = [&](float base) -> float {
+                    float2 lsum = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) emit_chunk(ch, base, lsum);
+                    return lsum.x + lsum.y;
+                };
+                auto mask_chunk = [&](int ch) {
+                    if (lim < kB) {  // causal diagonal / sequence tail / list tail
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (ch * 32 + jj >= lim) v[ch * 32 + jj] = 0xff800000u;  // -inf -> p = 0
+                    }
+                };
                 tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
                 tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
                 tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
                 tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
                 tmem_wait_ld();
-                if (lim < kB) {  // causal diagonal / sequence tail / list tail
 #pragma unroll
-                    for (int jj = 0; jj < kB; ++jj)
-                        if (jj >= lim) v[jj] = 0xff800000u;  // -inf -> p = 0
-                }
+                for (int ch = 0; ch < 4; ++ch) mask_chunk(ch);
                 if constexpr (MODE == TILEMASS) {
                     // exact normalised mass of this (query block, key tile):
                     // per-row sum with RECALL's final (max, sum), reduced over
@@ -480,27 +642,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_arrive(&S.bar_p_full[X]);
                     continue;
                 }
-                // P = 2^(s*c - base) as f16 over S columns [0, 64); returns the row sum
-                auto emit = [&](float base) -> float {
-                    float2 lsum = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 2) {
-                            const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
-                                                               __uint_as_float(v[ch * 32 + jj + 1])),
-                                                   c, -base);
-                            const float2 pp = (jj >> 1) % 16 < kPolyPairs
-                                                  ? ex2_poly2(x)
-                                                  : make_float2(ex2(x.x), ex2(x.y));
-                            lsum = fadd2(lsum, pp);
-                            pk[jj >> 1] = pack_half2(pp.x, pp.y);
-                        }
-                        tmem_st16(tS + ch * 16, pk);
-                    }
-                    return lsum.x + lsum.y;
-                };
                 if (it == 0) {
                     // first tile: the row max sets the base
                     const float mx = row_max128(v);
@@ -539,7 +680,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&S.bar_p_full[X]);
+                PROF(ps_comp += clock64() - ps_t1;)
             }
+            PROF(const long long t_epi0 = clock64();)
 
             // -------------------------------------------------------- epilogue
             if (kQkOnly<MODE>) {
@@ -554,30 +697,18 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
                 tc_fence_after();
             }
-            const bool valid_row = row < P.n;
-            const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
-            if (MODE == ANCHOR) {
+            if constexpr (MODE == ANCHOR) {
+                // acc_out = O * f (the state rescaled to the true max) leaves
+                // through shared memory so that the global stores are coalesced
+                // (a warp instruction covers 512 contiguous bytes instead of 32
+                // rows x 16 B)
+                const bool valid_row = row < P.n;
                 const float mt2 = m_raw * c;
-                const float f = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
-                float* acc = P.acc_out + rowoff;
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t v[32];
-                    tmem_ld32(tO + ch * 32, v);
-                    tmem_wait_ld();
-                    if (valid_row) {
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 4)
-                            *reinterpret_cast<float4*>(acc + ch * 32 + jj) = make_float4(
-                                __uint_as_float(v[jj]) * f, __uint_as_float(v[jj + 1]) * f,
-                                __uint_as_float(v[jj + 2]) * f, __uint_as_float(v[jj + 3]) * f);
-                    }
-                    __syncwarp();
-                }
+                const float so = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
                 const float m_nat = m_raw * P.inv_sqrt_d;
                 if (valid_row) {
                     P.m_out[static_cast<size_t>(h) * P.n + row] = m_nat;
-                    P.l_out[static_cast<size_t>(h) * P.n + row] = l * f;
+                    P.l_out[static_cast<size_t>(h) * P.n + row] = l * so;
                 }
                 if (P.msum != nullptr) {
                     float ms = valid_row ? m_nat : 0.f;
@@ -585,26 +716,45 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     for (int o = 16; o; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
                     if (lane == 0) S.red[X][0][quad] = ms;
                 }
-                if (P.qsum != nullptr) {
-                    // column r of this query tile, summed over its 128 rows (zero past n)
-                    const int col = r;
-                    const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes;
-                    const int chunk = (col & 63) >> 3, e = col & 7;
-                    float s = 0.f;
-                    for (int rr = 0; rr < kB; ++rr) {
-                        const __nv_bfloat16 x = *reinterpret_cast<const __nv_bfloat16*>(
-                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4) + e * 2);
-                        s += __bfloat162float(x);
+                // staging: this tile's Q buffer (its last QK has completed and the
+                // column sums are done), 128 rows x 64 f32 per half, 16-B chunks
+                // XOR-swizzled by row
+                if (P.qsum != nullptr && nX > 0) mbar_wait(&S.bar_qsum, 0);
+                float* stg = reinterpret_cast<float*>(S.q[X]);
+                const int rows_valid = min(kB, P.n - qx * kB);
+                const size_t gbase = (static_cast<size_t>(h) * P.n + qx * kB) * kD;
+                for (int half = 0; half < 2; ++half) {
+                    if (half) named_bar_sync(1 + X, 128);  // half 0 drained from the staging buffer
+                    uint32_t v[64];
+                    tmem_ld32(tO + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                    tmem_ld32(tO + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int ch = 0; ch < 16; ++ch)
+                        *reinterpret_cast<float4*>(stg + r * 64 + ((ch ^ (r & 15)) << 2)) = make_float4(
+                            __uint_as_float(v[4 * ch]) * so, __uint_as_float(v[4 * ch + 1]) * so,
+                            __uint_as_float(v[4 * ch + 2]) * so, __uint_as_float(v[4 * ch + 3]) * so);
+                    named_bar_sync(1 + X, 128);
+                    // thread r copies float4 i*128 + r (row idx/16, chunk idx%16): a
+                    // warp instruction spans two rows' 256 contiguous bytes
+                    const int ch = r & 15;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int rr = (i * kB + r) >> 4;
+                        const float4 o = *reinterpret_cast<const float4*>(stg + rr * 64 + ((ch ^ (rr & 15)) << 2));
+                        if (rr < rows_valid)
+                            *reinterpret_cast<float4*>(P.acc_out + gbase + static_cast<size_t>(rr) * kD +
+                                                       half * 64 + ch * 4) = o;
                     }
-                    P.qsum[(static_cast<size_t>(h) * P.T_m + qx) * kD + col] = s;
                 }
-                if (X == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-                else asm volatile("bar.sync 2, 128;" ::: "memory");
                 if (P.msum != nullptr && quad == 0 && lane == 0) {
+                    // S.red was written before the staging barriers above
                     P.msum[static_cast<size_t>(h) * P.T_m + qx] =
                         static_cast<double>(S.red[X][0][0]) + S.red[X][0][1] + S.red[X][0][2] + S.red[X][0][3];
                 }
             } else {
+            const bool valid_row = row < P.n;
+            const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
                 float fa = 0.f, fs = 1.f, inv = 0.f;
                 const float* acc_a = nullptr;
                 if (MODE == SPARSE) {
@@ -670,6 +820,16 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
             }
             }  // MODE != RECALL
+            PROF(if (lane == 0 && (warp == 4 || warp == 8)) {
+                const int o = warp == 4 ? 0 : 11;
+                atomicAdd(&g_prof[o], ps_wait);
+                atomicAdd(&g_prof[o + 1], ps_comp);
+                if (warp == 4) {
+                    atomicAdd(&g_prof[2], static_cast<unsigned long long>(nX));
+                    atomicAdd(&g_prof[7], clock64() - t_epi0);
+                    if (nX > 0) atomicAdd(&g_prof[8], ps_first - t_cta0);
+                }
+            })
         }
     }
 
@@ -677,6 +837,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     if (C > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
+    PROF(if (threadIdx.x == 0) {
+        atomicAdd(&g_prof[6], clock64() - t_cta0);
+        atomicAdd(&g_prof[9], 1ull);
+    })
 }
 
 // ------------------------------------------------------------------------ K2
@@ -1042,7 +1206,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     // fetched once per cluster (TMA multicast); needs every group complete
     // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
     P.cluster = 1;
-    if (MODE == SPARSE && P.T_m % P.step == 0) {
+    P.k_rows = static_cast<const uint8_t*>(k);
+    P.v16_rows = static_cast<const uint8_t*>(v16);
+    P.lsu = 0;
+    if (MODE == SPARSE) {
+        if (const char* env = getenv("AA_K3_GATHER")) P.lsu = env[0] == 'l' ? 1 : env[0] == 'a' ? 2 : 0;
+    }
+    if (MODE == SPARSE && !P.lsu && P.T_m % P.step == 0) {
         for (int c : {AA_CLUSTER_MAX, 2})
             if (ipg % c == 0) {
                 P.cluster = c;
@@ -1270,3 +1440,15 @@ cudaError_t fast_tile_mass(const FastArgs& f, const void* q, const void* k, floa
 }
 
 }  // namespace aa
+
+#ifdef AA_PROF
+extern "C" int aa_prof_read(unsigned long long* out, int reset) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, aa::g_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[16] = {};
+        if (cudaMemcpyToSymbol(aa::g_prof, z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return 0;
+}
+#endif

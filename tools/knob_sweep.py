@@ -58,6 +58,9 @@ def main():
             pipe(q, k, v, out=out, computed=computed)
         torch.cuda.synchronize()
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(a.reps)]
+        for row in evs:
+            for e in row:
+                e.record(stream)  # materialise the events (the library records them later)
         for r in range(a.reps):
             capi.set_stage_events(evs[r])
             pipe(q, k, v, out=out, computed=computed)
