@@ -40,6 +40,12 @@ constexpr int kD = 128;  // head dim
 constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
 constexpr int kLsuThreads = 64;     // K3 lsu mode: warps 2-3 gather the stripe rows
+// K ring depth of fa_pair (V keeps 2 stages): K(j + kKStages) can be fetched as
+// soon as QK_B(j) has read stage j — one more tile of lead for the gathers.
+#ifndef AA_K_STAGES
+#define AA_K_STAGES 2
+#endif
+constexpr int kKStages = AA_K_STAGES;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -117,10 +123,10 @@ struct FaParams {
 // Shared memory of fa_pair: two query tiles, 2-stage K and V rings.
 struct PairSmem {
     uint8_t q[2][kTileBytes];
-    uint8_t k[2][kTileBytes];
+    uint8_t k[kKStages][kTileBytes];
     uint8_t v[2][kTileBytes];
     uint64_t bar_q, bar_qsum;
-    uint64_t bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
+    uint64_t bar_k_full[kKStages], bar_k_empty[kKStages], bar_v_full[2], bar_v_empty[2];
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
     float red[2][2][4];
@@ -202,9 +208,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         mbar_init(&S.bar_q, 1);
         mbar_init(&S.bar_qsum, 64);
         const uint32_t fills = (MODE == SPARSE && P.lsu) ? kLsuThreads : 1;
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kKStages; ++b) {
             mbar_init(&S.bar_k_full[b], fills);
             mbar_init(&S.bar_k_empty[b], C);
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(&S.bar_v_full[b], fills);
             mbar_init(&S.bar_v_empty[b], C);
             mbar_init(&S.bar_s_full[b], 1);
@@ -263,23 +271,24 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
             for (int it = 0; it < ntiles; ++it) {
                 const int st = it & 1;
+                const int sk = it % kKStages;
                 int rk[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) rk[u] = kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
                 if (lane == 0) {
-                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
-                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
+                    if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
+                    mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
                 }
                 __syncwarp();
-                uint8_t* kd = S.k[st] + row0 * 128;
+                uint8_t* kd = S.k[sk] + row0 * 128;
                 if (gl) {
                     if (C > 1) {
-                        tma_gather4_mc(kd, &tmKg, &S.bar_k_full[st], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
-                        tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], cmask, 64, rk[0], rk[1],
+                        tma_gather4_mc(kd, &tmKg, &S.bar_k_full[sk], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[sk], cmask, 64, rk[0], rk[1],
                                        rk[2], rk[3]);
                     } else {
-                        tma_gather4(kd, &tmKg, &S.bar_k_full[st], 0, rk[0], rk[1], rk[2], rk[3]);
-                        tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[st], 64, rk[0], rk[1], rk[2],
+                        tma_gather4(kd, &tmKg, &S.bar_k_full[sk], 0, rk[0], rk[1], rk[2], rk[3]);
+                        tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[sk], 64, rk[0], rk[1], rk[2],
                                     rk[3]);
                     }
                 }
@@ -308,13 +317,14 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             for (int it = 0; it < ntiles; ++it) {
                 if (lane == 0) {
                     const int st = it & 1;
+                    const int sk = it % kKStages;
                     const int kt = kv_tile_of(MODE, it, wsb);
                     PROF(const long long t0 = clock64();)
-                    if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
+                    if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
                     PROF(atomicAdd(&g_prof[10], clock64() - t0);)
-                    mbar_expect_tx(&S.bar_k_full[st], kTileBytes);
-                    tma_load_3d(S.k[st], &tmK, &S.bar_k_full[st], 0, kt * kB, kvh);
-                    tma_load_3d(S.k[st] + kAtomBytes, &tmK, &S.bar_k_full[st], 64, kt * kB, kvh);
+                    mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
+                    tma_load_3d(S.k[sk], &tmK, &S.bar_k_full[sk], 0, kt * kB, kvh);
+                    tma_load_3d(S.k[sk] + kAtomBytes, &tmK, &S.bar_k_full[sk], 64, kt * kB, kvh);
                     if (!kQkOnly<MODE>) {
                         if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                         mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
@@ -338,9 +348,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             const uint32_t lv0 = sdesc_sw128_lo(smem_u32(S.v[0]), kAtomBytes);
             PROF(long long pw_p = 0, pw_k = 0, pw_v = 0;)
             auto qk = [&](int X, int j) {
-                const int st = j & 1;
+                const int st = j % kKStages;
                 PROF(const long long t0 = clock64();)
-                mbar_wait(&S.bar_k_full[st], (j >> 1) & 1);
+                mbar_wait(&S.bar_k_full[st], (j / kKStages) & 1);
                 PROF(pw_k += clock64() - t0;)
                 tc_fence_after();
                 if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
@@ -391,13 +401,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     if (j + 1 < nB) qk(1, j + 1);
                 }
                 release(&S.bar_v_empty[j & 1]);
-                if (j + 1 < ntiles) release(&S.bar_k_empty[(j + 1) & 1]);
+                if (j + 1 < ntiles) release(&S.bar_k_empty[(j + 1) % kKStages]);
             }
             if (C > 1) {
                 // every CTA's last releases have landed here before the exit
                 // cluster barrier, so no remote arrive can target a retired CTA
                 const int jl = ntiles - 1;
-                mbar_wait(&S.bar_k_empty[jl & 1], (jl >> 1) & 1);
+                mbar_wait(&S.bar_k_empty[jl % kKStages], (jl / kKStages) & 1);
                 mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
             }
             PROF(atomicAdd(&g_prof[3], pw_p); atomicAdd(&g_prof[4], pw_k); atomicAdd(&g_prof[5], pw_v);)
@@ -444,12 +454,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             const size_t kstride = static_cast<size_t>(P.kv_row_rows) * 256;
             for (int it = 0; it < ntiles; ++it) {
                 const int st = it & 1;
+                const int sk = it % kKStages;
                 const int base = it * kB;
                 const int e0 = base + wr + lane, e1 = e0 + 32;
                 const uint32_t a0 = list[e0 < count ? e0 : base];
                 const uint32_t a1 = list[e1 < count ? e1 : base];
-                if (it >= 2) mbar_wait(&S.bar_k_empty[st], ((it >> 1) - 1) & 1);
-                const uint32_t kd = smem_u32(S.k[st]) + chunk_off;
+                if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
+                const uint32_t kd = smem_u32(S.k[sk]) + chunk_off;
 #pragma unroll 8
                 for (int i = 0; i < 32; ++i) {
                     const int rho = 2 * i + hsel;  // row within this warp's 64
@@ -458,7 +469,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     cp_async16(kd + r * 128 + ((c8 ^ (r & 7)) << 4), kbase + j * kstride);
                 }
                 if (P.lsu == 2) {
-                    cp_async_arrive_noinc(&S.bar_k_full[st]);
+                    cp_async_arrive_noinc(&S.bar_k_full[sk]);
                 } else {
                     cp_async_commit();
                     if (it >= 1) {  // V(it-1) landed
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     cp_async_commit();
                     cp_async_wait<1>();  // K(it) landed
                     fence_proxy_async_smem();
-                    mbar_arrive(&S.bar_k_full[st]);
+                    mbar_arrive(&S.bar_k_full[sk]);
                 }
             }
             if (ntiles > 0 && P.lsu == 1) {
@@ -1166,6 +1177,7 @@ cudaError_t make_map_gather(CUtensorMap* m, const void* base, CUtensorMapDataTyp
 }
 
 constexpr size_t kSmemBytes = sizeof(PairSmem) + 1024;
+static_assert(kSmemBytes <= 232448, "fa_pair shared memory exceeds 227 KB");
 
 template <int MODE>
 cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const void* v16,
