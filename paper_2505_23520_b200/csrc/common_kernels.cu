@@ -1,35 +1,68 @@
 // Kernels shared by both arithmetic paths.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace aa {
 namespace {
 
-// Ordered compaction of one (head, group) selection row: each thread owns one
-// 32-candidate word per pass, a block-wide exclusive scan of the word
-// popcounts places its keys, and keys are emitted in ascending order — the
-// sorted, unique list of StripeIndex (R/include/anchorattn/stripe_identify.hpp:17-19)
-// without atomics.  grid (groups, hq), block 1024.
-__global__ void __launch_bounds__(1024) k_compact(Geo geo, const uint32_t* __restrict__ bits,
-                                                  int64_t words_per_row,
-                                                  const int64_t* __restrict__ offsets, int64_t cap,
-                                                  uint32_t* __restrict__ indices,
-                                                  int32_t* __restrict__ counts) {
-    __shared__ int warp_tot[32];
-    __shared__ int warp_excl[32];
-    const int64_t g = blockIdx.x, h = blockIdx.y;
-    const int64_t groups = gridDim.x;
+// Ordered compaction of the (head, group) selection rows into the sorted,
+// unique lists of StripeIndex (R/include/anchorattn/stripe_identify.hpp:17-19),
+// without atomics.  One block per row (heaviest groups first), kCompactWarps
+// warps, each owning a contiguous run of bit-words: pass 1 counts the run's
+// selected keys, a block scan gives each run its output offset, pass 2 walks
+// the run 32 words (1024 candidates) at a time, staging the step's keys in
+// shared memory in ascending order and writing them out contiguously.  Global traffic: the
+// bits (twice, the second time from L2) plus 4 B per selected key.
+constexpr int kCompactWarps = 8;
+
+__global__ void __launch_bounds__(kCompactWarps * 32)
+    k_compact(Geo geo, int64_t hq, const uint32_t* __restrict__ bits, int64_t words_per_row,
+              const int64_t* __restrict__ offsets, int64_t cap, uint32_t* __restrict__ indices,
+              int32_t* __restrict__ counts) {
+    __shared__ uint32_t stage[kCompactWarps][1024];
+    __shared__ int run_excl[kCompactWarps + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t groups = geo.groups();
+    const int64_t g = groups - 1 - blockIdx.x / hq, h = blockIdx.x % hq;
     const int64_t len = geo.middle_len(g);
     const int64_t words = (len + 31) >> 5;
     const uint32_t* row = bits + (h * groups + g) * words_per_row;
     uint32_t* dst = indices + h * cap + offsets[g];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int64_t base = 0;
-    for (int64_t w0 = 0; w0 < words; w0 += blockDim.x) {
-        const int64_t w = w0 + threadIdx.x;
-        uint32_t word = w < words ? row[w] : 0u;
-        if (w == words - 1 && (len & 31)) word &= (1u << (len & 31)) - 1u;
+    const int64_t per = (words + kCompactWarps * 32 - 1) / (kCompactWarps * 32) * 32;
+    const int64_t s0 = min(words, wid * per), s1 = min(words, s0 + per);
+    auto word_at = [&](int64_t w) -> uint32_t {
+        if (w >= s1) return 0u;
+        uint32_t x = row[w];
+        if (w == words - 1 && (len & 31)) x &= (1u << (len & 31)) - 1u;
+        return x;
+    };
+    // pass 1: keys selected in this warp's run
+    int cnt = 0;
+#pragma unroll 8
+    for (int64_t w = s0 + lane; w < s1; w += 32) cnt += __popc(word_at(w));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) run_excl[wid + 1] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        run_excl[0] = 0;
+        for (int i = 1; i <= kCompactWarps; ++i) run_excl[i] += run_excl[i - 1];
+        counts[h * groups + g] = run_excl[kCompactWarps];
+    }
+    __syncthreads();
+    // pass 2: ordered, coalesced writes (next word loaded one step ahead):
+    // a warp scan of the word popcounts places each lane's keys in shared
+    // memory in ascending order, then the warp writes the step's keys out
+    // contiguously
+    uint32_t* stg = stage[wid];
+    int64_t base = run_excl[wid];
+    uint32_t nxt = word_at(s0 + lane);
+    for (int64_t w0 = s0; w0 < s1; w0 += 32) {
+        uint32_t word = nxt;
+        nxt = word_at(w0 + 32 + lane);
         const int c = __popc(word);
         int incl = c;
 #pragma unroll
@@ -37,31 +70,20 @@ __global__ void __launch_bounds__(1024) k_compact(Geo geo, const uint32_t* __res
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        if (lane == 31) warp_tot[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const int t = lane < static_cast<int>(blockDim.x >> 5) ? warp_tot[lane] : 0;
-            int s = t;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_excl[lane] = s - t;
-            if (lane == 31) warp_tot[0] = s;  // block total (read after barrier)
-        }
-        __syncthreads();
-        int64_t pos = base + warp_excl[wid] + (incl - c);
-        const uint32_t key0 = static_cast<uint32_t>(geo.b_kv + (w << 5));
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        // highest set bit first, written from the end of this lane's slots
+        int pos = incl;
+        const uint32_t key0 = static_cast<uint32_t>(geo.b_kv + ((w0 + lane) << 5));
         while (word) {
-            const int b = __ffs(word) - 1;
-            dst[pos++] = key0 + static_cast<uint32_t>(b);
-            word &= word - 1u;
+            const int b = 31 - __clz(word);
+            stg[--pos] = key0 + static_cast<uint32_t>(b);
+            word ^= 1u << b;
         }
-        base += warp_tot[0];
-        __syncthreads();
+        __syncwarp();
+        for (int j = lane; j < total; j += 32) dst[base + j] = stg[j];
+        __syncwarp();
+        base += total;
     }
-    if (threadIdx.x == 0) counts[h * groups + g] = static_cast<int32_t>(base);
 }
 
 __global__ void k_computed(Geo geo, int64_t covered, const int32_t* __restrict__ counts,
@@ -82,28 +104,58 @@ __global__ void k_add_u64(int64_t hq, int64_t covered, const unsigned long long*
     if (h < hq) computed[h] = covered + static_cast<int64_t>(taken[h]);
 }
 
-__global__ void k_offsets(Geo geo, int64_t* __restrict__ offsets) {
+// offsets[g] = sum of middle_len over the groups before g (capacity layout):
+// one thread per group and a block scan (one block covers up to 1024 groups,
+// i.e. 2M tokens at step 16; beyond that a per-thread loop).
+__global__ void __launch_bounds__(1024) k_offsets(Geo geo, int64_t* __restrict__ offsets) {
+    __shared__ int64_t warp_sum[32];
     const int64_t G = geo.groups();
-    int64_t off = 0;
-    for (int64_t g = 0; g < G; ++g) {
-        offsets[g] = off;
-        off += geo.middle_len(g);
+    if (G >= 1024) {
+        for (int64_t g = threadIdx.x; g <= G; g += blockDim.x) {
+            int64_t off = 0;
+            for (int64_t h = 0; h < g; ++h) off += geo.middle_len(h);
+            offsets[g] = off;
+        }
+        return;
     }
-    offsets[G] = off;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    int64_t x = t < G ? geo.middle_len(t) : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t v = warp_sum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        warp_sum[lane] = v;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t incl = x + (wid > 0 ? warp_sum[wid - 1] : 0);
+    if (t < G) offsets[t + 1] = incl;
+    if (t == 0) offsets[0] = 0;
 }
 
 }  // namespace
 
 cudaError_t launch_offsets(const Geo& geo, int64_t* offsets, cudaStream_t s) {
-    k_offsets<<<1, 1, 0, s>>>(geo, offsets);
+    k_offsets<<<1, 1024, 0, s>>>(geo, offsets);
     return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const Geo& geo, int64_t hq, const uint32_t* bits,
                            int64_t words_per_row, const int64_t* offsets, int64_t cap,
                            uint32_t* indices, int32_t* counts, cudaStream_t s) {
-    k_compact<<<dim3(static_cast<unsigned>(geo.groups()), static_cast<unsigned>(hq)), 1024, 0,
-                s>>>(geo, bits, words_per_row, offsets, cap, indices, counts);
+    const int64_t rows = geo.groups() * hq;
+    if (rows == 0) return cudaSuccess;
+    k_compact<<<static_cast<unsigned>(rows), kCompactWarps * 32, 0, s>>>(geo, hq, bits, words_per_row,
+                                                                        offsets, cap, indices, counts);
     return cudaGetLastError();
 }
 

@@ -858,57 +858,88 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 // Alg. 2 (R/src/stripe_identify.cpp:31-46) on the tensor cores.
 //
 // For one KV head, the pooled queries of its GQA query heads form the rows
-// r = g * rep + hh (group-major) of an A operand; 128 rows per CTA (one
-// M-tile).  q_bar is f32 in the reference; it enters the MMA as an exact-ish
-// split q_bar = hi + lo (two bf16 terms, residual ~2^-17 |q_bar|), so
+// r = g * rep + hh (group-major) of an A operand, 128 rows per M-tile.  q_bar
+// is f32 in the reference; it enters the MMA as an exact-ish split
+// q_bar = hi + lo (two bf16 terms, residual ~2^-17 |q_bar|), so
 // S = hi K^T + lo K^T is the f32 score to ~1e-5 — far inside the +-1e-3
-// selection band — while K streams from HBM once per (head, M-tile).
-// Each TMEM lane holds one (head, group) row, so its thread assembles the
-// 32-bit selection words of 32 consecutive keys directly (no ballot).
+// selection band.  Each TMEM lane holds one (head, group) row, so its thread
+// assembles the 32-bit selection words of 32 consecutive keys directly.
 //
-// grid (chunks of key tiles, M-tiles, hkv); 192 threads: warp 0 TMA,
-// warp 1 MMA, warps 2-5 threshold + bit words.  K ring of 2 stages, 2 TMEM
-// accumulators.
-constexpr int kIdChunk = 16;  // key tiles per CTA
+// One CTA owns a KV head and a PAIR of M-tiles (both A operands resident,
+// 128 KB) and walks every J-th chunk of 8 key tiles of that head, so each K
+// tile is read from HBM exactly once and feeds the MMAs of both M-tiles (the
+// first M-tile holds the earlier groups and stops at its shorter middle
+// region).  Strided chunks balance the two-tile and one-tile parts of the
+// key range across the J CTAs of a head.  K streams through a 3-stage TMA
+// ring; TMEM holds 2 M-tiles x 2 accumulators.  320 threads: warp 0 TMA,
+// warp 1 MMA (+ TMEM), warps 2-9 threshold + bit words (warps 2-5 M-tile 0,
+// 6-9 M-tile 1; thread <-> TMEM lane <-> (head, group) row).
+constexpr int kIdThreads = 320;
+constexpr int kIdChunk = 8;    // key tiles per chunk
+constexpr int kIdStages = 3;   // K ring depth
 
 struct IdSmem {
-    uint8_t a_hi[kTileBytes];
-    uint8_t a_lo[kTileBytes];
-    uint8_t k[2][kTileBytes];
-    uint64_t bar_a, bar_k_full[2], bar_k_empty[2], bar_s_full[2], bar_s_empty[2];
+    uint8_t a[2][2][kTileBytes];  // [M-tile of the pair][hi, lo]
+    uint8_t k[kIdStages][kTileBytes];
+    uint64_t bar_a;
+    uint64_t bar_k_full[kIdStages], bar_k_empty[kIdStages];
+    uint64_t bar_s_full[2][2], bar_s_empty[2][2];  // [M-tile][accumulator]
     uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+struct IdWork {
+    Geo geo;
+    int rep, n_mt, n_pairs, J;
+};
+
+// Key tiles of M-tile mt: up to the widest middle region of its groups.
+__device__ __forceinline__ int id_tiles(const IdWork& w, int mt) {
+    if (mt >= w.n_mt) return 0;
+    const int groups = static_cast<int>(w.geo.groups());
+    const int g_last = min(groups - 1, ((mt + 1) * kB - 1) / w.rep);
+    const int64_t span = w.geo.middle_end(g_last) - w.geo.b_kv;
+    return span > 0 ? static_cast<int>((span + kB - 1) / kB) : 0;
+}
+
+__global__ void __launch_bounds__(kIdThreads, 1)
     k_identify_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmK,
-                  Geo geo, int rep, int rows_pad, const double* __restrict__ anchor, double theta,
+                  const IdWork w, const double* __restrict__ anchor, double theta,
                   uint32_t* __restrict__ bits, int64_t words_per_row) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     IdSmem& S = *reinterpret_cast<IdSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kvh = blockIdx.z;
-    const int mt = blockIdx.y;
-    const int groups = static_cast<int>(geo.groups());
-    // key tiles relevant to this M-tile: up to the widest middle region of its groups
-    const int g_last = min(groups - 1, ((mt + 1) * kB - 1) / rep);
-    const int64_t span = geo.middle_end(g_last) - geo.b_kv;
-    const int tiles_total = span > 0 ? static_cast<int>((span + kB - 1) / kB) : 0;
-    const int t0 = blockIdx.x * kIdChunk;
-    const int nt = max(0, min(kIdChunk, tiles_total - t0));
-    if (nt == 0) return;
+    PROF(const long long t_cta0 = clock64();)
+    const int groups = static_cast<int>(w.geo.groups());
+    const int j0 = blockIdx.x % w.J;
+    const int pair = (blockIdx.x / w.J) % w.n_pairs;
+    const int kvh = blockIdx.x / (w.J * w.n_pairs);
+    const int mt0 = 2 * pair;
+    const int T0 = id_tiles(w, mt0), T1 = id_tiles(w, mt0 + 1);
+    const int T = max(T0, T1);
+    const int nchunks = (T + kIdChunk - 1) / kIdChunk;
+    const int my_chunks = nchunks > j0 ? (nchunks - j0 + w.J - 1) / w.J : 0;
+    if (my_chunks == 0) return;
+    const bool two = T1 > 0;
+    // this CTA's i-th chunk, alternating from both ends of its list: chunks
+    // where both M-tiles are live (tensor-heavy) interleave with one-tile
+    // chunks (HBM-heavy), so at any moment the CTAs load both pipes
+    auto chunk_at = [&](int i) { return j0 + w.J * ((i & 1) ? my_chunks - 1 - (i >> 1) : (i >> 1)); };
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_a, 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kIdStages; ++b) {
             mbar_init(&S.bar_k_full[b], 1);
             mbar_init(&S.bar_k_empty[b], 1);
-            mbar_init(&S.bar_s_full[b], 1);
-            mbar_init(&S.bar_s_empty[b], 128);
         }
+        for (int m = 0; m < 2; ++m)
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&S.bar_s_full[m][b], 1);
+                mbar_init(&S.bar_s_empty[m][b], 128);
+            }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&S.tmem_base, 256);
+    if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -916,100 +947,137 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(&S.bar_a, 2 * kTileBytes);
-            const int arow = mt * kB;
-            tma_load_3d(S.a_hi, &tmA, &S.bar_a, 0, arow, 2 * kvh);
-            tma_load_3d(S.a_hi + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh);
-            tma_load_3d(S.a_lo, &tmA, &S.bar_a, 0, arow, 2 * kvh + 1);
-            tma_load_3d(S.a_lo + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh + 1);
-            for (int i = 0; i < nt; ++i) {
-                const int b = i & 1;
-                if (i >= 2) mbar_wait(&S.bar_k_empty[b], ((i >> 1) - 1) & 1);
-                mbar_expect_tx(&S.bar_k_full[b], kTileBytes);
-                const int key0 = static_cast<int>(geo.b_kv) + (t0 + i) * kB;
-                tma_load_3d(S.k[b], &tmK, &S.bar_k_full[b], 0, key0, kvh);
-                tma_load_3d(S.k[b] + kAtomBytes, &tmK, &S.bar_k_full[b], 64, key0, kvh);
+            mbar_expect_tx(&S.bar_a, (two ? 4 : 2) * kTileBytes);
+            for (int m = 0; m < (two ? 2 : 1); ++m) {
+                const int arow = (mt0 + m) * kB;
+                tma_load_3d(S.a[m][0], &tmA, &S.bar_a, 0, arow, 2 * kvh);
+                tma_load_3d(S.a[m][0] + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh);
+                tma_load_3d(S.a[m][1], &tmA, &S.bar_a, 0, arow, 2 * kvh + 1);
+                tma_load_3d(S.a[m][1] + kAtomBytes, &tmA, &S.bar_a, 64, arow, 2 * kvh + 1);
+            }
+            int nk = 0;
+            for (int ci = 0; ci < my_chunks; ++ci) {
+                const int c = chunk_at(ci);
+                const int t_end = min(T, (c + 1) * kIdChunk);
+                for (int t = c * kIdChunk; t < t_end; ++t, ++nk) {
+                    const int b = nk % kIdStages;
+                    PROF(const long long t0 = clock64();)
+                    if (nk >= kIdStages) mbar_wait(&S.bar_k_empty[b], ((nk / kIdStages) - 1) & 1);
+                    PROF(atomicAdd(&g_prof[0], clock64() - t0);)
+                    mbar_expect_tx(&S.bar_k_full[b], kTileBytes);
+                    const int key0 = static_cast<int>(w.geo.b_kv) + t * kB;
+                    tma_load_3d(S.k[b], &tmK, &S.bar_k_full[b], 0, key0, kvh);
+                    tma_load_3d(S.k[b] + kAtomBytes, &tmK, &S.bar_k_full[b], 64, key0, kvh);
+                }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t ah = smem_u32(S.a_hi), al = smem_u32(S.a_lo);
+            constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
+            const uint32_t la0 = sdesc_sw128_lo(smem_u32(S.a[0][0]), 16);
+            const uint32_t lk0 = sdesc_sw128_lo(smem_u32(S.k[0]), 16);
             mbar_wait(&S.bar_a, 0);
-            for (int i = 0; i < nt; ++i) {
-                const int b = i & 1;
-                mbar_wait(&S.bar_k_full[b], (i >> 1) & 1);
-                if (i >= 2) mbar_wait(&S.bar_s_empty[b], ((i >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t kb = smem_u32(S.k[b]);
-                const uint32_t d_tmem = tmem + b * 128;
+            int nk = 0;
+            int ns[2] = {0, 0};
+            for (int ci = 0; ci < my_chunks; ++ci) {
+                const int c = chunk_at(ci);
+                const int t_end = min(T, (c + 1) * kIdChunk);
+                for (int t = c * kIdChunk; t < t_end; ++t, ++nk) {
+                    const int b = nk % kIdStages;
+                    PROF(const long long t0 = clock64();)
+                    mbar_wait(&S.bar_k_full[b], (nk / kIdStages) & 1);
+                    PROF(atomicAdd(&g_prof[1], clock64() - t0); atomicAdd(&g_prof[9], 1ull);)
+                    const uint32_t lk = lk0 + b * (kTileBytes >> 4);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-                    mma_ss(d_tmem, sdesc_sw128(ah + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
-                           kIdescQK, kk > 0 ? 1u : 0u);
-                }
+                    for (int m = 0; m < 2; ++m) {
+                        if (t >= (m ? T1 : T0)) continue;  // this M-tile's groups end earlier
+                        const int sb = ns[m] & 1;
+                        PROF(const long long t0 = clock64();)
+                        if (ns[m] >= 2) mbar_wait(&S.bar_s_empty[m][sb], ((ns[m] >> 1) - 1) & 1);
+                        PROF(atomicAdd(&g_prof[2], clock64() - t0);)
+                        tc_fence_after();
+                        const uint32_t lhi = la0 + m * (2 * kTileBytes >> 4), llo = lhi + (kTileBytes >> 4);
+                        const uint32_t d_tmem = tmem + (2 * m + sb) * 128;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-                    mma_ss(d_tmem, sdesc_sw128(al + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
-                           kIdescQK, 1u);
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
+                            mma_ss(d_tmem, kDescHi | (lhi + off), kDescHi | (lk + off), kIdescQK,
+                                   kk > 0 ? 1u : 0u);
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
+                            mma_ss(d_tmem, kDescHi | (llo + off), kDescHi | (lk + off), kIdescQK, 1u);
+                        }
+                        mma_commit(&S.bar_s_full[m][sb]);
+                        ++ns[m];
+                    }
+                    mma_commit(&S.bar_k_empty[b]);
                 }
-                mma_commit(&S.bar_s_full[b]);
-                mma_commit(&S.bar_k_empty[b]);
             }
         }
         __syncwarp();
     } else {
-        const int quad = warp & 3;
+        const int m = (warp - 2) >> 2;  // M-tile of the pair
+        const int quad = warp & 3;      // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;
-        const int grow = mt * kB + r;
-        const int g = grow / rep, hh = kvh * rep + grow % rep;
-        const bool valid = grow < groups * rep;
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const int Tm = m ? T1 : T0;
+        const int grow = (mt0 + m) * kB + r;
+        const int g = grow / w.rep, hh = kvh * w.rep + grow % w.rep;
+        const bool valid = grow < groups * w.rep;
         int64_t mend = 0;
         float thr = 0.f;
         if (valid) {
-            mend = geo.middle_end(g);
+            mend = w.geo.middle_end(g);
             const double ref = anchor ? anchor[static_cast<int64_t>(hh) * groups + g] : 0.0;
             // keep iff ref - s*inv_sqrt_d <= theta  <=>  s >= (ref - theta) * sqrt(d)
             thr = static_cast<float>((ref - theta) * sqrt(static_cast<double>(kD)));
         }
-        uint32_t* rowbits = bits + (static_cast<int64_t>(hh) * groups + g) * words_per_row;
-        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        for (int i = 0; i < nt; ++i) {
-            const int b = i & 1;
-            mbar_wait(&S.bar_s_full[b], (i >> 1) & 1);
-            tc_fence_after();
-            const int64_t key0 = geo.b_kv + static_cast<int64_t>(t0 + i) * kB;
-            uint32_t w[4];
+        uint32_t* rowbits = bits + (static_cast<int64_t>(valid ? hh : 0) * groups + (valid ? g : 0)) * words_per_row;
+        int ns = 0;
+        for (int ci = 0; ci < my_chunks; ++ci) {
+            const int c = chunk_at(ci);
+            const int t_end = min(Tm, (c + 1) * kIdChunk);
+            for (int t = c * kIdChunk; t < t_end; ++t, ++ns) {
+                const int sb = ns & 1;
+                PROF(const long long t0 = clock64();)
+                mbar_wait(&S.bar_s_full[m][sb], (ns >> 1) & 1);
+                PROF(const long long t1 = clock64(); if (lane == 0 && (warp == 2 || warp == 6)) atomicAdd(&g_prof[3], t1 - t0);)
+                tc_fence_after();
+                const int64_t key0 = w.geo.b_kv + static_cast<int64_t>(t) * kB;
+                uint32_t wd[4];
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tmem + b * 128 + lane_off + ch * 32, v);
-                tmem_wait_ld();
-                uint32_t word = 0;
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + (2 * m + sb) * 128 + lane_off + ch * 32, v);
+                    tmem_wait_ld();
+                    uint32_t word = 0;
 #pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    word |= (__uint_as_float(v[c]) >= thr ? 1u : 0u) << c;
-                const int64_t kfirst = key0 + ch * 32;
-                if (kfirst + 32 > mend) {
-                    const int64_t keep = mend - kfirst;
-                    word = keep <= 0 ? 0u : (keep >= 32 ? word : word & ((1u << keep) - 1u));
+                    for (int cc = 0; cc < 32; ++cc) word |= (__uint_as_float(v[cc]) >= thr ? 1u : 0u) << cc;
+                    const int64_t kfirst = key0 + ch * 32;
+                    if (kfirst + 32 > mend) {
+                        const int64_t keep = mend - kfirst;
+                        word = keep <= 0 ? 0u : (keep >= 32 ? word : word & ((1u << keep) - 1u));
+                    }
+                    wd[ch] = word;
                 }
-                w[ch] = word;
-            }
-            tc_fence_before();
-            mbar_arrive(&S.bar_s_empty[b]);
-            if (valid && key0 < mend) {
-                const int64_t word0 = (key0 - geo.b_kv) >> 5;
-                *reinterpret_cast<uint4*>(rowbits + word0) = make_uint4(w[0], w[1], w[2], w[3]);
+                tc_fence_before();
+                mbar_arrive(&S.bar_s_empty[m][sb]);
+                if (valid && key0 < mend) {
+                    const int64_t word0 = (key0 - w.geo.b_kv) >> 5;
+                    *reinterpret_cast<uint4*>(rowbits + word0) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                }
+                PROF(if (lane == 0 && (warp == 2 || warp == 6)) { atomicAdd(&g_prof[4], clock64() - t1); atomicAdd(&g_prof[5], 1ull); })
             }
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, 256);
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    PROF(if (threadIdx.x == 0) { atomicAdd(&g_prof[6], clock64() - t_cta0); atomicAdd(&g_prof[7], 1ull); })
 }
 
 // q_bar (f32 [hq, G, d]) -> A operand rows r = g*rep + hh of KV head kvh as a
@@ -1338,19 +1406,30 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
         return e;
     }
     constexpr size_t smem = sizeof(IdSmem) + 1024;
+    static_assert(smem <= 232448, "k_identify_tc shared memory exceeds 227 KB");
     static bool attr = false;
+    static int sms = 0;
     if (!attr) {
         if ((e = cudaFuncSetAttribute(k_identify_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)))) {
             cudaFreeAsync(split, s);
             return e;
         }
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         attr = true;
     }
-    const unsigned chunks = static_cast<unsigned>((tiles + kIdChunk - 1) / kIdChunk);
-    k_identify_tc<<<dim3(chunks, static_cast<unsigned>(rows_pad / kB), static_cast<unsigned>(f.hkv)),
-                    kThreads, smem, s>>>(ta, tk, f.geo, static_cast<int>(f.rep), rows_pad, anchor,
-                                         f.theta, bits, words_per_row);
+    IdWork w;
+    w.geo = f.geo;
+    w.rep = static_cast<int>(f.rep);
+    w.n_mt = rows_pad / kB;
+    w.n_pairs = (w.n_mt + 1) / 2;
+    const int heads_pairs = static_cast<int>(f.hkv) * w.n_pairs;
+    const int nchunks = static_cast<int>((tiles + kIdChunk - 1) / kIdChunk);
+    w.J = std::max(1, std::min(nchunks, (sms > 0 ? sms : 148) / std::max(1, heads_pairs)));
+    const unsigned grid = static_cast<unsigned>(heads_pairs * w.J);
+    k_identify_tc<<<grid, kIdThreads, smem, s>>>(ta, tk, w, anchor, f.theta, bits, words_per_row);
     e = cudaGetLastError();
     cudaFreeAsync(split, s);
     return e;
