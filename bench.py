@@ -265,7 +265,7 @@ def run_ours(args):
         pipe(q, k, v, out=out, computed=computed)
     torch.cuda.synchronize()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
     for row in evs:
         for e in row:
             e.record(stream)  # materialise the CUDA events
@@ -288,6 +288,7 @@ def run_ours(args):
     ms_local = t0.elapsed_time(t1) / args.steps
     stage_ms = [statistics.mean(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps))
                 for i in range(5)]
+    k2_kernel_ms = statistics.mean(evs[s][6].elapsed_time(evs[s][7]) for s in range(args.steps))
 
     print(f"[bench] rank {rank}: {ms_local:.3f} ms/layer-shard, stages "
           + ", ".join(f"{nm}={t:.3f}" for nm, t in zip(capi.STAGES, stage_ms)), file=sys.stderr,
@@ -301,9 +302,12 @@ def run_ours(args):
 
     # roofline of the dominant kernel (this rank's launches)
     peaks = measured_peaks()
-    tensor_peak = peaks.get("bf16_tflops", 1590.0)
+    # K3 runs inside a long back-to-back step (the whole chain, K steps): the
+    # sustained tensor peak is the denominator (B200_PROFILING.md); the burst
+    # fraction is reported beside it
+    tensor_peak_burst = peaks.get("bf16_tflops", 1590.0)
+    tensor_peak = peaks.get("bf16_tflops_sustained", tensor_peak_burst)
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "measured burst (MEASURED_PEAKS.json)" if peaks else "fallback (B200_PROFILING.md)"
     k1_flops = 4.0 * D * hq_local * covered
     k3_flops = 4.0 * D * (comp_local - hq_local * covered)
     kernels = {
@@ -320,8 +324,14 @@ def run_ours(args):
     G = capi.lib().aa_group_count(args.n, C.byref(c_cfg))
     max_mid = max(0, capi.lib().aa_middle_end_token(G - 1, C.byref(c_cfg), args.n) - 128)
     k2_bytes = kv_local * max_mid * D * 2 + hq_local * G * (D * 4 + 8)
-    kernels["k2_identify"] = {"ms": stage_ms[2], "bytes": k2_bytes,
-                              "gbs": k2_bytes / (stage_ms[2] * 1e-3) / 1e9}
+    kernels["k2_identify"] = {"ms": k2_kernel_ms, "bytes": k2_bytes,
+                              "gbs": k2_bytes / (k2_kernel_ms * 1e-3) / 1e9,
+                              "frac_hbm": k2_bytes / (k2_kernel_ms * 1e-3) / 1e9 / hbm_peak,
+                              "hbm_peak_gbs": hbm_peak,
+                              "note": "k_identify_tc alone (events 6->7); bound: HBM"}
+    kernels["k2_stage"] = {"ms": stage_ms[2], "bytes": k2_bytes,
+                           "gbs": k2_bytes / (stage_ms[2] * 1e-3) / 1e9,
+                           "note": "pool + q_bar split + identify + offsets + compaction"}
     dom = max(("k1_anchor", "k3_sparse"), key=lambda kname: kernels[kname]["ms"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -335,7 +345,10 @@ def run_ours(args):
     roofline = {"bound": "tensor", "kernel": dom, "achieved": kernels[dom]["tflops"],
                 "peak": tensor_peak, "unit": "TFLOP/s",
                 "frac": kernels[dom]["tflops"] / tensor_peak, "traffic": traffic,
-                "peak_source": peak_src,
+                "peak_source": ("measured sustained bf16 (MEASURED_PEAKS.json bf16_tflops_sustained; "
+                                "the kernel runs inside a long back-to-back step)" if peaks else
+                                "fallback (B200_PROFILING.md)"),
+                "frac_of_burst_peak": kernels[dom]["tflops"] / tensor_peak_burst,
                 "work": f"4*d*positions = {kernels[dom]['flops']:.4e} FLOP per launch"}
 
     # recall of the selection at 128k: one dense QK pass (RECALL kernel) over
@@ -432,7 +445,9 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 8 * args.steps,
+            # per step: V->f16, K1, pool, q_bar split, K2 identify, offsets,
+            # compaction, K3, computed counts
+            "gpu_launches": 9 * args.steps,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -193,7 +193,8 @@ aa_status aa_dense_tile_mass(const aa_problem* p, const void* q, const void* k,
 /* Stage timing for profilers/benchmarks: while set, the fast path of
  * aa_anchor_attention records events[i] (cudaEvent_t) on its stream at the
  * stage boundaries 0 start | 1 V->f16 | 2 K1 anchor | 3 pool + K2 identify +
- * compaction | 4 K3 sparse | 5 stats.  Per calling thread; NULL disables. */
+ * compaction | 4 K3 sparse | 5 stats, and (count >= 8) 6 / 7 right before /
+ * after the K2 identify kernel itself.  Per calling thread; NULL disables. */
 aa_status aa_set_stage_events(void* const* events, int count);
 
 /* Plumbing for host callers that do not link the CUDA runtime themselves. */

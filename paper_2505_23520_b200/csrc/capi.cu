@@ -27,6 +27,13 @@ thread_local int g_nevents = 0;
 void mark(int i, cudaStream_t st) {
     if (i < g_nevents && g_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(g_events[i]), st);
 }
+}  // namespace
+
+namespace aa {
+void stage_mark(int i, cudaStream_t st) { mark(i, st); }
+}  // namespace aa
+
+namespace {
 
 aa_status fail(aa_status s, const std::string& msg) {
     g_err = msg;

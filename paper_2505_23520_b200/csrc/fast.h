@@ -17,6 +17,9 @@ struct FastArgs {
     double theta;
 };
 
+// Records stage event i of aa_set_stage_events on `st` (no-op when unset).
+void stage_mark(int i, cudaStream_t st);
+
 // V (bf16, strided) -> packed f16 copy [hkv, n, d] consumed by the PV MMAs.
 cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s);
 // K1 — Alg. 1 anchor pass (tile list {0} ∪ [wsb(g), qb]); writes f32 m, l,

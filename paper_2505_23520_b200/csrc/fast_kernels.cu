@@ -241,8 +241,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
             }
         }
+#ifdef AA_K3_ACC_PREFETCH
         if (MODE == SPARSE && lane == 0 && ntiles > 0) {
             // the epilogue's K1 state rows (acc: 64 KB per query tile) -> L2 now
+            // (measured: no epilogue gain, +0.9 GB of K/V gather re-reads)
             for (int X = 0; X < (hasB ? 2 : 1); ++X) {
                 const int r0 = (X ? qB : qA) * kB;
                 const int rows = min(kB, P.n - r0);
@@ -250,6 +252,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                                  static_cast<uint32_t>(rows) * kD * 4);
             }
         }
+#endif
         if (MODE == SPARSE && !P.lsu) {
             // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
             // column halves, for K and for V).  Standalone CTA: 32 lanes cover
@@ -1429,7 +1432,9 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     const int nchunks = static_cast<int>((tiles + kIdChunk - 1) / kIdChunk);
     w.J = std::max(1, std::min(nchunks, (sms > 0 ? sms : 148) / std::max(1, heads_pairs)));
     const unsigned grid = static_cast<unsigned>(heads_pairs * w.J);
+    stage_mark(6, s);  // K2 kernel alone: events 6 -> 7 (inside stage 3)
     k_identify_tc<<<grid, kIdThreads, smem, s>>>(ta, tk, w, anchor, f.theta, bits, words_per_row);
+    stage_mark(7, s);
     e = cudaGetLastError();
     cudaFreeAsync(split, s);
     return e;

@@ -57,7 +57,7 @@ def main():
         for _ in range(3):
             pipe(q, k, v, out=out, computed=computed)
         torch.cuda.synchronize()
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(a.reps)]
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(a.reps)]
         for row in evs:
             for e in row:
                 e.record(stream)  # materialise the events (the library records them later)
@@ -74,7 +74,8 @@ def main():
             same = True
         else:
             same = bool(torch.equal(out, ref))
-        print(json.dumps({"env": dict(s), "ms": statistics.median(tot), "min_ms": min(tot),
+        k2k = statistics.median(evs[r][6].elapsed_time(evs[r][7]) for r in range(a.reps))
+        print(json.dumps({"env": dict(s), "ms": statistics.median(tot), "min_ms": min(tot), "k2_kernel_ms": k2k,
                           "stages": dict(zip(capi.STAGES, st)), "out_equal_first": same}),
               flush=True)
 

@@ -31,26 +31,31 @@ KEYS = {
 
 
 def raw(rep):
+    """One record per profiled launch of the report."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    res = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
-    stalls = {}
-    for h, u, v in zip(hdr, units, vals):
-        if h in KEYS:
-            res[KEYS[h]] = f"{v} {u}".strip()
-        if h.startswith("smsp__average_warp_latency_issue_stalled_") or \
-           h.startswith("smsp__pcsamp_warps_issue_stalled_"):
-            try:
-                stalls[h.split("stalled_")[1]] = float(v.replace(",", ""))
-            except ValueError:
-                pass
-    top = sorted(stalls.items(), key=lambda kv: -kv[1])[:8]
-    res["top_stalls"] = top
-    return res
+    hdr, units = rows[0], rows[1]
+    recs = []
+    for vals in rows[2:]:
+        if len(vals) != len(hdr):
+            continue
+        res = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
+        stalls = {}
+        for h, u, v in zip(hdr, units, vals):
+            if h in KEYS:
+                res[KEYS[h]] = f"{v} {u}".strip()
+            if h.startswith("smsp__average_warp_latency_issue_stalled_") or \
+               h.startswith("smsp__pcsamp_warps_issue_stalled_"):
+                try:
+                    stalls[h.split("stalled_")[1]] = float(v.replace(",", ""))
+                except ValueError:
+                    pass
+        res["top_stalls"] = sorted(stalls.items(), key=lambda kv: -kv[1])[:8]
+        recs.append(res)
+    return recs
 
 
 if __name__ == "__main__":
-    recs = [raw(p) for p in sys.argv[1:]]
+    recs = [r for p in sys.argv[1:] for r in raw(p)]
     print(json.dumps(recs, indent=1))
