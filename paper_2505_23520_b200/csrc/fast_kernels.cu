@@ -37,7 +37,6 @@ using namespace sm100;
 
 constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
-constexpr int kThreads = 192;       // K2 identify CTA
 constexpr int kPairThreads = 384;   // fa_pair CTA
 constexpr int kLsuThreads = 64;     // K3 lsu mode: warps 2-3 gather the stripe rows
 // K ring depth of fa_pair (V keeps 2 stages): K(j + kKStages) can be fetched as
@@ -46,6 +45,21 @@ constexpr int kLsuThreads = 64;     // K3 lsu mode: warps 2-3 gather the stripe 
 #define AA_K_STAGES 2
 #endif
 constexpr int kKStages = AA_K_STAGES;
+// Each query tile's softmax warpgroup issues its own MMAs (PV_X(j), QK_X(j+1))
+// right after a named barrier over its 128 threads, instead of handing P to a
+// separate MMA warp through an mbarrier (no wake-up hop, no coupling of the
+// two tiles' MMA streams through one issuing thread).
+#ifndef AA_TILE_ISSUE
+#define AA_TILE_ISSUE 0
+#endif
+constexpr bool kTileIssue = AA_TILE_ISSUE != 0;
+// The two tiles' softmax sections strictly alternate (named-barrier tokens,
+// FA4-style): while one tile computes exponentials the tensor pipe works on
+// the other tile's PV / QK, and the two never contend for MUFU.
+#ifndef AA_PINGPONG
+#define AA_PINGPONG 0
+#endif
+constexpr bool kPingPong = AA_PINGPONG != 0;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -130,6 +144,7 @@ struct PairSmem {
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
     float red[2][2][4];
+    long long t_arrive[2];  // AA_PROF: softmax -> MMA hand-off stamps
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
@@ -208,13 +223,16 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         mbar_init(&S.bar_q, 1);
         mbar_init(&S.bar_qsum, 64);
         const uint32_t fills = (MODE == SPARSE && P.lsu) ? kLsuThreads : 1;
+        // with per-tile issue, each tile's issuer releases every stage once
+        // (twice when the other tile does not use it)
+        const uint32_t releases = (kTileIssue ? 2 : 1) * C;
         for (int b = 0; b < kKStages; ++b) {
             mbar_init(&S.bar_k_full[b], fills);
-            mbar_init(&S.bar_k_empty[b], C);
+            mbar_init(&S.bar_k_empty[b], releases);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&S.bar_v_full[b], fills);
-            mbar_init(&S.bar_v_empty[b], C);
+            mbar_init(&S.bar_v_empty[b], releases);
             mbar_init(&S.bar_s_full[b], 1);
             mbar_init(&S.bar_p_full[b], 128);
             mbar_init(&S.bar_o_done[b], 1);
@@ -341,7 +359,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     } else if (warp == 1) {
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0 && ntiles > 0) {
+        if (!kTileIssue && lane == 0 && ntiles > 0) {
             // SW128 descriptors: the high word (SBO 1024, version, layout) is a
             // constant, the low word = start address >> 4 | LBO >> 4 << 16
             constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
@@ -372,12 +390,15 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 const int st = j & 1;
                 PROF(const long long t0 = clock64();)
                 mbar_wait(&S.bar_p_full[X], j & 1);
-                PROF(const long long t1 = clock64(); pw_p += t1 - t0;)
+                PROF(const long long t1 = clock64(); pw_p += t1 - t0;
+                     atomicAdd(&g_prof[13], t1 - *reinterpret_cast<volatile long long*>(&S.t_arrive[X]));
+                     atomicAdd(&g_prof[14], 1ull);)
                 if (kQkOnly<MODE>) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 PROF(pw_v += clock64() - t1;)
                 tc_fence_after();
                 if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
+                PROF(const long long t_iss = clock64();)
                 const uint32_t lv = lv0 + st * (kTileBytes >> 4);
                 const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
@@ -385,6 +406,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mma_ts(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
                            (j > 0 || kk > 0) ? 1u : 0u);
                 mma_commit(&S.bar_o_done[X]);
+                PROF(atomicAdd(&g_prof[15], clock64() - t_iss);)
             };
             // a stage is released to every producer of the cluster that fills it
             auto release = [&](uint64_t* bar) {
@@ -535,6 +557,73 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 wstart_x = min(wsbx * kB, P.n);
             }
 
+            // per-tile MMA issue (kTileIssue): lane 0 of the tile's first warp
+            const bool issuer = kTileIssue && quad == 0 && lane == 0;
+            const int nO = X ? nA : nB;  // the other tile's tile count
+            constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
+            const uint32_t lqX = sdesc_sw128_lo(smem_u32(S.q[X]), 16);
+            const uint32_t lk0 = sdesc_sw128_lo(smem_u32(S.k[0]), 16);
+            const uint32_t lv0 = sdesc_sw128_lo(smem_u32(S.v[0]), kAtomBytes);
+            // stage t is released by each tile that uses it (twice by this tile
+            // if the other tile does not), to every producer of the cluster
+            auto release = [&](uint64_t* bar, int t) {
+                const int times = t < nO ? 1 : 2;
+                for (int i = 0; i < times; ++i) {
+                    if (C > 1) mma_commit_mc(bar, cmask); else mma_commit(bar);
+                }
+            };
+            auto issue_qk = [&](int t) {
+                const int st = t % kKStages;
+                mbar_wait(&S.bar_k_full[st], (t / kKStages) & 1);
+                tc_fence_after();
+                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
+                const uint32_t lk = lk0 + st * (kTileBytes >> 4);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
+                    mma_ss(tmem + X * 128, kDescHi | (lqX + off), kDescHi | (lk + off), kIdescQK,
+                           kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&S.bar_s_full[X]);
+                release(&S.bar_k_empty[st], t);
+            };
+            auto issue_pv = [&](int t) {
+                const int st = t & 1;
+                mbar_wait(&S.bar_v_full[st], (t >> 1) & 1);
+                tc_fence_after();
+                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
+                const uint32_t lv = lv0 + st * (kTileBytes >> 4);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ts(tmem + 256 + X * 128, tmem + X * 128 + kk * 8, kDescHi | (lv + kk * (2048 >> 4)),
+                           kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+                mma_commit(&S.bar_o_done[X]);
+                release(&S.bar_v_empty[st], t);
+            };
+            // P(it) is in TMEM (or S(it) consumed): hand the tile to the tensor pipe
+            auto tile_done = [&](int it) {
+                if constexpr (kTileIssue) {
+                    named_bar_sync(1 + X, 128);
+                    if (issuer) {
+                        tc_fence_after();
+                        if (!kQkOnly<MODE>) issue_pv(it);
+                        if (it + 1 < nX) issue_qk(it + 1);
+                        if (it + 1 == nX && C > 1 && X == 0) {
+                            // every CTA's last releases have landed before the exit
+                            // cluster barrier (no remote arrive targets a retired CTA)
+                            const int jl = ntiles - 1;
+                            mbar_wait(&S.bar_k_empty[jl % kKStages], (jl / kKStages) & 1);
+                            mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
+                        }
+                    }
+                } else {
+                    mbar_arrive(&S.bar_p_full[X]);
+                }
+            };
+            if (issuer && nX > 0) {
+                mbar_wait(&S.bar_q, 0);
+                issue_qk(0);
+            }
             PROF(long long ps_wait = 0, ps_comp = 0, ps_t1 = 0, ps_first = 0;)
             for (int it = 0; it < nX; ++it) {
                 int lim;
@@ -549,6 +638,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_s_full[X], it & 1);
                 PROF(ps_t1 = clock64(); ps_wait += ps_t1 - ps_t0; if (it == 0) ps_first = ps_t1;)
                 tc_fence_after();
+                // ping-pong token: A(it) after B(it-1), B(it) after A(it)
+                if (kPingPong && !kQkOnly<MODE>) {
+                    if (X == 0 ? (it >= 1 && it - 1 < nB) : (it < nA))
+                        named_bar_sync(X == 0 ? 3 : 4, 256);
+                }
                 // single pass: the whole S row in registers
                 uint32_t v[128];
                 // P = 2^(s*c - base) as f16 over S columns [16 ch, 16 ch + 16)
@@ -605,7 +699,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         rm = (acc2.x + acc2.y) / st.y;
                     }
                     tc_fence_before();
-                    mbar_arrive(&S.bar_p_full[X]);  // S consumed
+                    tile_done(it);  // S consumed
 #pragma unroll
                     for (int sh = 16; sh; sh >>= 1) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
                     if (lane == 0) S.red[X][it & 1][quad] = rm;
@@ -653,7 +747,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     l += la.x + la.y;
                     l_sel += ls.x + ls.y;
                     tc_fence_before();
-                    mbar_arrive(&S.bar_p_full[X]);
+                    tile_done(it);
                     continue;
                 }
                 if (it == 0) {
@@ -693,8 +787,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(&S.bar_p_full[X]);
+                PROF(if (quad == 0 && lane == 0) *reinterpret_cast<volatile long long*>(&S.t_arrive[X]) = clock64();)
                 PROF(ps_comp += clock64() - ps_t1;)
+                if (kPingPong && !kQkOnly<MODE>) {
+                    if (X == 0 ? (it < nB) : (it + 1 < nA)) named_bar_arrive(X == 0 ? 4 : 3, 256);
+                }
+                tile_done(it);
             }
             PROF(const long long t_epi0 = clock64();)
 

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 EXP = os.path.join(ROOT, "exp")
 
 
-def build_tree(tree, tag):
+def build_tree(tree, tag, extra_flags=()):
     pkg = os.path.join(tree, "paper_2505_23520_b200")
     csrc = os.path.join(pkg, "csrc")
     nvcc = "/usr/local/cuda/bin/nvcc"
@@ -23,7 +23,7 @@ def build_tree(tree, tag):
     flags = arch + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                     "-I", os.path.join(tree, "include"), "-I", csrc]
     cus = sorted(f for f in os.listdir(csrc) if f.endswith(".cu"))
-    for variant, extra in (("", []), ("_prof", ["-DAA_PROF"])):
+    for variant, extra in (("", list(extra_flags)), ("_prof", ["-DAA_PROF"] + list(extra_flags))):
         objs = []
         procs = []
         for cu in cus:
@@ -52,7 +52,11 @@ def main():
     finally:
         subprocess.run(["git", "-C", ROOT, "worktree", "remove", "--force", wt])
     build_tree(ROOT, "B")
-    print("built exp/libA.so exp/libB.so (+ _prof)")
+    # optional third variant: the working tree with extra nvcc flags (AB_C_FLAGS)
+    cflags = os.environ.get("AB_C_FLAGS", "").split()
+    if cflags:
+        build_tree(ROOT, "C", cflags)
+    print("built exp/libA.so exp/libB.so (+ _prof)" + (f", exp/libC.so ({' '.join(cflags)})" if cflags else ""))
 
 
 if __name__ == "__main__":

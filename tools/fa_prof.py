@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 PROF_LIB = os.path.join(ROOT, "exp", "libanchorattn_b200_prof.so")
 SLOTS = ["smA_wait_s", "smA_compute", "smA_tiles", "mma_wait_p", "mma_wait_k", "mma_wait_v",
          "cta_cycles", "epilogue", "prologue", "ctas", "prod_wait_empty", "smB_wait_s",
-         "smB_compute"]
+         "smB_compute", "handoff_p_to_mma", "handoffs", "pv_issue"]
 
 
 def build():
@@ -69,6 +69,8 @@ def main():
                 continue
             row[s + "_per_cta"] = round(v[i] / ctas)
         row["smA_compute_per_tile"] = round(v[1] / tiles)
+        row["p_to_mma_wake_avg"] = round(v[13] / max(1, v[14]))
+        row["pv_issue_avg"] = round(v[15] / max(1, v[14]))
         row["smA_wait_per_tile"] = round(v[0] / tiles)
         row["lib"] = os.path.basename(a.lib)
         print(json.dumps(row), flush=True)
