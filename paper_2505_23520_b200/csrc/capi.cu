@@ -484,7 +484,7 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
     mark(1, st);
     AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
-                            static_cast<double*>(L.msum), st));
+                            static_cast<double*>(L.msum), st, /*acc_f16=*/true));
     mark(2, st);
     AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
                           static_cast<double*>(L.msum), static_cast<double*>(L.anchor),
@@ -500,7 +500,7 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
     AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
                             static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
-                            false, out, out_dtype, st));
+                            false, out, out_dtype, st, /*acc_f16=*/true));
     mark(4, st);
     if (computed)
         AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions,

@@ -24,8 +24,11 @@ void stage_mark(int i, cudaStream_t st);
 cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s);
 // K1 — Alg. 1 anchor pass (tile list {0} ∪ [wsb(g), qb]); writes f32 m, l,
 // acc and the per-q-block partial sums qsum [hq, T_m, d] / msum [hq, T_m].
+// acc_f16: acc is written as f16 acc / l (the fused chain's hand-off to K3,
+// half the bytes; fast_sparse must be given the same flag).
 cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v16, float* m,
-                        float* l, float* acc, float* qsum, double* msum, cudaStream_t s);
+                        float* l, float* acc, float* qsum, double* msum, cudaStream_t s,
+                        bool acc_f16 = false);
 // Per-group pooled query (f32) and anchor (f64) from K1 partials (or from
 // q / m when the partials are NULL).
 cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const float* qsum,
@@ -38,7 +41,8 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
 cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v16,
                         const float* m, const float* l, const float* acc,
                         const uint32_t* indices, const int32_t* counts, const int64_t* offsets,
-                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, cudaStream_t s);
+                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, cudaStream_t s,
+                        bool acc_f16 = false);
 cudaError_t fast_finalize(const FastArgs& f, const float* l, const float* acc, void* out,
                           aa_dtype out_dtype, cudaStream_t s);
 // D — dense causal FlashAttention-style tcgen05 kernel (the speed baseline).

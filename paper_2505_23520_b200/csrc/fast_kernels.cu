@@ -123,6 +123,10 @@ struct FaParams {
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
     int item0;    // first work item of this launch (K3 split launches)
     int lsu;      // K3: gather the stripe rows with cp.async (warps 2-3) instead of TMA gather4
+    // K1 -> K3 hand-off format: 0 = acc f32 unnormalised (AnchorState::acc,
+    // the stage API); 1 = f16 acc / l (normalised, |.| <= max|v|: half the
+    // bytes both ways; the fused chain)
+    int acc_f16;
     const uint8_t* k_rows;    // K base (rows of d bf16, 256 B) for the LSU gathers
     const uint8_t* v16_rows;  // packed f16 V [hkv, n, d]
     // RECALL inputs / output
@@ -817,6 +821,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 const bool valid_row = row < P.n;
                 const float mt2 = m_raw * c;
                 const float so = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt2);
+                // staged values: O * so (acc, f32 hand-off) or O / l (f16 hand-off)
+                const float sv = P.acc_f16 ? 1.f / l : so;
                 const float m_nat = m_raw * P.inv_sqrt_d;
                 if (valid_row) {
                     P.m_out[static_cast<size_t>(h) * P.n + row] = m_nat;
@@ -844,8 +850,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 #pragma unroll
                     for (int ch = 0; ch < 16; ++ch)
                         *reinterpret_cast<float4*>(stg + r * 64 + ((ch ^ (r & 15)) << 2)) = make_float4(
-                            __uint_as_float(v[4 * ch]) * so, __uint_as_float(v[4 * ch + 1]) * so,
-                            __uint_as_float(v[4 * ch + 2]) * so, __uint_as_float(v[4 * ch + 3]) * so);
+                            __uint_as_float(v[4 * ch]) * sv, __uint_as_float(v[4 * ch + 1]) * sv,
+                            __uint_as_float(v[4 * ch + 2]) * sv, __uint_as_float(v[4 * ch + 3]) * sv);
                     named_bar_sync(1 + X, 128);
                     // thread r copies float4 i*128 + r (row idx/16, chunk idx%16): a
                     // warp instruction spans two rows' 256 contiguous bytes
@@ -854,9 +860,17 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     for (int i = 0; i < 16; ++i) {
                         const int rr = (i * kB + r) >> 4;
                         const float4 o = *reinterpret_cast<const float4*>(stg + rr * 64 + ((ch ^ (rr & 15)) << 2));
-                        if (rr < rows_valid)
-                            *reinterpret_cast<float4*>(P.acc_out + gbase + static_cast<size_t>(rr) * kD +
-                                                       half * 64 + ch * 4) = o;
+                        if (rr < rows_valid) {
+                            const size_t ge = gbase + static_cast<size_t>(rr) * kD + half * 64 + ch * 4;
+                            if (P.acc_f16) {
+                                uint2 w;
+                                w.x = pack_half2(o.x, o.y);
+                                w.y = pack_half2(o.z, o.w);
+                                *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(P.acc_out) + ge) = w;
+                            } else {
+                                *reinterpret_cast<float4*>(P.acc_out + ge) = o;
+                            }
+                        }
                     }
                 }
                 if (P.msum != nullptr && quad == 0 && lane == 0) {
@@ -878,6 +892,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
                     inv = 1.f / (la * fa + l * fs);
                     acc_a = P.acc_in + rowoff;
+                    if (P.acc_f16) fa *= la;  // acc_in holds acc / l
                 } else {
                     inv = 1.f / l;
                 }
@@ -895,7 +910,20 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         float o[32];
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) o[jj] = __uint_as_float(v[jj]) * fs;
-                        if (MODE == SPARSE) {
+                        if (MODE == SPARSE && P.acc_f16) {
+                            const __half* ah = reinterpret_cast<const __half*>(P.acc_in) + rowoff + ch * 32;
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 8) {
+                                const uint4 raw = *reinterpret_cast<const uint4*>(ah + jj);
+                                const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const float2 a = __half22float2(h2[u]);
+                                    o[jj + 2 * u] += a.x * fa;
+                                    o[jj + 2 * u + 1] += a.y * fa;
+                                }
+                            }
+                        } else if (MODE == SPARSE) {
 #pragma unroll
                             for (int jj = 0; jj < 32; jj += 4) {
                                 const float4 a = *reinterpret_cast<const float4*>(acc_a + ch * 32 + jj);
@@ -1462,8 +1490,9 @@ cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStre
 }
 
 cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v16, float* m,
-                        float* l, float* acc, float* qsum, double* msum, cudaStream_t s) {
+                        float* l, float* acc, float* qsum, double* msum, cudaStream_t s, bool acc_f16) {
     FaParams P{};
+    P.acc_f16 = acc_f16 ? 1 : 0;
     P.m_out = m;
     P.l_out = l;
     P.acc_out = acc;
@@ -1541,8 +1570,10 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
 cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v16,
                         const float* m, const float* l, const float* acc,
                         const uint32_t* indices, const int32_t* counts, const int64_t* offsets,
-                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, cudaStream_t s) {
+                        int64_t cap, bool csr, void* out, aa_dtype out_dtype, cudaStream_t s,
+                        bool acc_f16) {
     FaParams P{};
+    P.acc_f16 = acc_f16 ? 1 : 0;
     P.m_in = m;
     P.l_in = l;
     P.acc_in = acc;

@@ -170,7 +170,9 @@ def test_theta_extremes_at_32k():
     torch.cuda.synchronize()
     pl = c.plan(c.make_problem(q, k, c.BlockConfig()))
     assert int(comp.max()) == pl.covered_positions
-    assert torch.allclose(none, fin, atol=1e-6, rtol=1e-5)
+    # the fused chain hands the anchor state to K3 as f16 acc / l (f16 carries
+    # 11 significant bits: relative rounding <= 2^-11)
+    assert torch.allclose(none, fin, atol=1e-5, rtol=2 ** -10)
 
 
 def test_selection_monotone_in_theta():
@@ -211,7 +213,12 @@ def test_stage_api_equals_fused_chain():
     out, comp2 = c.sparse(q, k, v, st, idx, counts, cfg)
     torch.cuda.synchronize()
     assert torch.equal(comp, comp2)
-    assert torch.equal(fused, out)
+    # the fused chain hands K1's state to K3 as f16 acc / l (half the bytes);
+    # the stage API keeps AnchorState's f32 acc: same selection, outputs equal
+    # to f16 rounding of the anchor part
+    err = (fused - out).abs().max().item()
+    rel = ((fused - out).norm() / out.norm()).item()
+    assert err <= 5e-3 and rel <= 3e-4, (err, rel)
 
 
 @pytest.mark.parametrize("n,step,theta", [(4096, 16, 12.0), (2048, 2, 10.0), (3000, 4, 14.0)])
