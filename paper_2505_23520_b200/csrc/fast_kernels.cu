@@ -1182,9 +1182,19 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                     uint32_t v[32];
                     tmem_ld32(tmem + (2 * m + sb) * 128 + lane_off + ch * 32, v);
                     tmem_wait_ld();
-                    uint32_t word = 0;
+                    // bit cc = (s_cc >= thr): the sign bit of s - thr (+0 when
+                    // equal) shifted in from the top, highest key first, so a
+                    // FADD2 and one funnel shift per key; the word holds the
+                    // rejected keys and is inverted once
+                    uint32_t neg = 0;
 #pragma unroll
-                    for (int cc = 0; cc < 32; ++cc) word |= (__uint_as_float(v[cc]) >= thr ? 1u : 0u) << cc;
+                    for (int cc = 30; cc >= 0; cc -= 2) {
+                        const float2 dd = fadd2(make_float2(__uint_as_float(v[cc]), __uint_as_float(v[cc + 1])),
+                                                make_float2(-thr, -thr));
+                        neg = __funnelshift_l(__float_as_uint(dd.y), neg, 1);
+                        neg = __funnelshift_l(__float_as_uint(dd.x), neg, 1);
+                    }
+                    uint32_t word = ~neg;
                     const int64_t kfirst = key0 + ch * 32;
                     if (kfirst + 32 > mend) {
                         const int64_t keep = mend - kfirst;
