@@ -148,7 +148,6 @@ struct PairSmem {
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
     float red[2][2][4];
-    long long t_arrive[2];  // AA_PROF: softmax -> MMA hand-off stamps
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
@@ -394,15 +393,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 const int st = j & 1;
                 PROF(const long long t0 = clock64();)
                 mbar_wait(&S.bar_p_full[X], j & 1);
-                PROF(const long long t1 = clock64(); pw_p += t1 - t0;
-                     atomicAdd(&g_prof[13], t1 - *reinterpret_cast<volatile long long*>(&S.t_arrive[X]));
-                     atomicAdd(&g_prof[14], 1ull);)
+                PROF(const long long t1 = clock64(); pw_p += t1 - t0;)
                 if (kQkOnly<MODE>) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 PROF(pw_v += clock64() - t1;)
                 tc_fence_after();
                 if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
-                PROF(const long long t_iss = clock64();)
                 const uint32_t lv = lv0 + st * (kTileBytes >> 4);
                 const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
@@ -410,7 +406,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mma_ts(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
                            (j > 0 || kk > 0) ? 1u : 0u);
                 mma_commit(&S.bar_o_done[X]);
-                PROF(atomicAdd(&g_prof[15], clock64() - t_iss);)
             };
             // a stage is released to every producer of the cluster that fills it
             auto release = [&](uint64_t* bar) {
@@ -772,6 +767,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     const float mx2 = mx * c;
                     const bool redo = mx2 > m_used + 8.f;
                     if (__any_sync(0xffffffffu, redo)) {  // tcgen05.ld/st are warp-collective
+                        PROF(if (lane == 0 && warp == 4) atomicAdd(&g_prof[13], 1ull);)
                         const float alpha = redo ? ex2(m_used - mx2) : 1.f;
                         if (redo) m_used = mx2;
                         l = l * alpha + emit(m_used);
@@ -791,7 +787,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 }
                 tmem_wait_st();
                 tc_fence_before();
-                PROF(if (quad == 0 && lane == 0) *reinterpret_cast<volatile long long*>(&S.t_arrive[X]) = clock64();)
                 PROF(ps_comp += clock64() - ps_t1;)
                 if (kPingPong && !kQkOnly<MODE>) {
                     if (X == 0 ? (it < nB) : (it + 1 < nA)) named_bar_arrive(X == 0 ? 4 : 3, 256);

@@ -69,8 +69,8 @@ def main():
                 continue
             row[s + "_per_cta"] = round(v[i] / ctas)
         row["smA_compute_per_tile"] = round(v[1] / tiles)
-        row["p_to_mma_wake_avg"] = round(v[13] / max(1, v[14]))
-        row["pv_issue_avg"] = round(v[15] / max(1, v[14]))
+        row["redo_per_tile_warp4"] = round(v[13] / tiles, 4)
+
         row["smA_wait_per_tile"] = round(v[0] / tiles)
         row["lib"] = os.path.basename(a.lib)
         print(json.dumps(row), flush=True)
