@@ -60,6 +60,13 @@ constexpr bool kTileIssue = AA_TILE_ISSUE != 0;
 #define AA_PINGPONG 0
 #endif
 constexpr bool kPingPong = AA_PINGPONG != 0;
+// K3 (TMA gathers): K rows are gathered by warp 0 and V rows by warp 3, each
+// at its own pace, instead of one loop that blocks on V's free stage before
+// it can fetch the next K tile.
+#ifndef AA_KV_SPLIT
+#define AA_KV_SPLIT 1
+#endif
+constexpr bool kKvSplit = AA_KV_SPLIT != 0;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -250,6 +257,48 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // register split (per warpgroup, inside each role branch): the producer /
     // MMA warpgroup needs few registers, the two softmax warpgroups hold a
     // whole S row (128 f32) each.
+    // K3 split gathers: one warp streams the K rows, another the V rows of
+    // every stripe tile (gather4: 4 rows x 128 B per instruction, x 2 column
+    // halves); in a cluster of C each CTA gathers rows [crank*128/C, +128/C)
+    // of a tile and multicasts them to the C CTAs.
+    auto gather_split = [&](bool isK) {
+        const int lanes = 32 / C;
+        const bool gl = lane < lanes;
+        const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
+        const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
+        for (int it = 0; it < ntiles; ++it) {
+            const int st = isK ? it % kKStages : it & 1;
+            const int ph = isK ? it / kKStages : it >> 1;
+            const int depth = isK ? kKStages : 2;
+            int r[4];
+            const int base = it * kB;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = base + row0 + u;
+                const int j = gl ? static_cast<int>(list[e < count ? e : base]) : 0;
+                r[u] = isK ? kvh * P.kv_head_rows + j * P.kv_row_rows : vh + j;
+            }
+            uint64_t* full = isK ? &S.bar_k_full[st] : &S.bar_v_full[st];
+            uint64_t* empty = isK ? &S.bar_k_empty[st] : &S.bar_v_empty[st];
+            if (lane == 0) {
+                if (it >= depth) mbar_wait(empty, (ph - 1) & 1);
+                mbar_expect_tx(full, kTileBytes);
+            }
+            __syncwarp();
+            uint8_t* dst = (isK ? S.k[st] : S.v[st]) + row0 * 128;
+            const CUtensorMap* tm = isK ? &tmKg : &tmVg;
+            if (gl) {
+                if (C > 1) {
+                    tma_gather4_mc(dst, tm, full, cmask, 0, r[0], r[1], r[2], r[3]);
+                    tma_gather4_mc(dst + kAtomBytes, tm, full, cmask, 64, r[0], r[1], r[2], r[3]);
+                } else {
+                    tma_gather4(dst, tm, full, 0, r[0], r[1], r[2], r[3]);
+                    tma_gather4(dst + kAtomBytes, tm, full, 64, r[0], r[1], r[2], r[3]);
+                }
+            }
+        }
+    };
+
     if (warp == 0) {
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ producer
@@ -274,7 +323,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
 #endif
-        if (MODE == SPARSE && !P.lsu) {
+        if (MODE == SPARSE && !P.lsu && kKvSplit) {
+            gather_split(true);
+        } else if (MODE == SPARSE && !P.lsu) {
             // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
             // column halves, for K and for V).  Standalone CTA: 32 lanes cover
             // the 128 rows; in a cluster of C, this CTA covers rows
@@ -439,6 +490,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         __syncwarp();
     } else if (warp < 4) {
         setmaxnreg_dec<56>();  // warps 2-3: LSU gathers of K3 (lsu mode), K1 column sums
+        if (MODE == SPARSE && !P.lsu && kKvSplit && warp == 3) gather_split(false);
         if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
             // pooled-query partials (avgpool_rows, R/src/matrix.cpp:44-65): column
             // sums of each query tile over its 128 rows (TMA zero-fills rows past
