@@ -67,6 +67,13 @@ constexpr bool kPingPong = AA_PINGPONG != 0;
 #define AA_KV_SPLIT 1
 #endif
 constexpr bool kKvSplit = AA_KV_SPLIT != 0;
+// The same split for the contiguous K/V tiles of K1 / dense (V loads on warp 3,
+// K1's column sums on warp 2 alone): measured neutral-to-negative (K1 +2%),
+// off.
+#ifndef AA_KV_SPLIT_TILES
+#define AA_KV_SPLIT_TILES 0
+#endif
+constexpr bool kKvSplitTiles = AA_KV_SPLIT_TILES != 0;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
-        mbar_init(&S.bar_qsum, 64);
+        mbar_init(&S.bar_qsum, kKvSplitTiles ? 32 : 64);
         const uint32_t fills = (MODE == SPARSE && P.lsu) ? kLsuThreads : 1;
         // with per-tile issue, each tile's issuer releases every stage once
         // (twice when the other tile does not use it)
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
                     tma_load_3d(S.k[sk], &tmK, &S.bar_k_full[sk], 0, kt * kB, kvh);
                     tma_load_3d(S.k[sk] + kAtomBytes, &tmK, &S.bar_k_full[sk], 64, kt * kB, kvh);
-                    if (!kQkOnly<MODE>) {
+                    if (!kQkOnly<MODE> && !kKvSplitTiles) {
                         if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                         mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
                         tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
@@ -491,27 +498,43 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     } else if (warp < 4) {
         setmaxnreg_dec<56>();  // warps 2-3: LSU gathers of K3 (lsu mode), K1 column sums
         if (MODE == SPARSE && !P.lsu && kKvSplit && warp == 3) gather_split(false);
-        if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
+        if (MODE != SPARSE && !kQkOnly<MODE> && kKvSplitTiles && warp == 3 && lane == 0) {
+            // V tiles at their own pace (the K tiles come from warp 0)
+            for (int it = 0; it < ntiles; ++it) {
+                const int st = it & 1;
+                const int kt = kv_tile_of(MODE, it, wsb);
+                if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
+                mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
+                tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
+                tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
+            }
+        }
+        if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0 && (warp == 2 || !kKvSplitTiles)) {
             // pooled-query partials (avgpool_rows, R/src/matrix.cpp:44-65): column
             // sums of each query tile over its 128 rows (TMA zero-fills rows past
-            // n), summed in row order; thread t owns columns 2t, 2t+1.  Runs
-            // beside the main loop, off the epilogue's critical path.
+            // n), summed in row order; each thread owns column pairs (2 pairs on
+            // warp 2 alone when warp 3 loads V).  Runs beside the main loop, off
+            // the epilogue's critical path.
             const int t = threadIdx.x - 64;
-            const int col = 2 * t;
-            const int chunk = (col & 63) >> 3, e = col & 7;
+            constexpr int kPairsPerThread = kKvSplitTiles ? 2 : 1;
             mbar_wait(&S.bar_q, 0);
             for (int X = 0; X < (hasB ? 2 : 1); ++X) {
-                const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes + e * 2;
-                float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                for (int pp = 0; pp < kPairsPerThread; ++pp) {
+                    const int col = 2 * (t * kPairsPerThread + pp);
+                    const int chunk = (col & 63) >> 3, e = col & 7;
+                    const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes + e * 2;
+                    float s0 = 0.f, s1 = 0.f;
 #pragma unroll 16
-                for (int rr = 0; rr < kB; ++rr) {
-                    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(
-                        atom + rr * 128 + ((chunk ^ (rr & 7)) << 4));
-                    s0 += __low2float(x);
-                    s1 += __high2float(x);
+                    for (int rr = 0; rr < kB; ++rr) {
+                        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(
+                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+                        s0 += __low2float(x);
+                        s1 += __high2float(x);
+                    }
+                    *reinterpret_cast<float2*>(P.qsum + (static_cast<size_t>(h) * P.T_m + (X ? qB : qA)) * kD +
+                                               col) = make_float2(s0, s1);
                 }
-                *reinterpret_cast<float2*>(P.qsum + (static_cast<size_t>(h) * P.T_m + (X ? qB : qA)) * kD + col) =
-                    make_float2(s0, s1);
             }
             mbar_arrive(&S.bar_qsum);  // the epilogue reuses the Q tiles as staging
         }
