@@ -1486,14 +1486,8 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
             return e;
         attr_set[MODE] = true;
     }
-#ifndef AA_CLUSTER_MAX
-#define AA_CLUSTER_MAX 4
-#endif
     const int ipg = (P.step + 1) / 2;
     const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
-    // K3: cluster the pairs of one (head, group) so each gathered tile is
-    // fetched once per cluster (TMA multicast); needs every group complete
-    // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
     P.cluster = 1;
     P.k_rows = static_cast<const uint8_t*>(k);
     P.v16_rows = static_cast<const uint8_t*>(v16);
@@ -1501,9 +1495,17 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     if (MODE == SPARSE) {
         if (const char* env = getenv("AA_K3_GATHER")) P.lsu = env[0] == 'l' ? 1 : env[0] == 'a' ? 2 : 0;
     }
+    // K3: cluster the pairs of one (head, group) so each gathered tile is
+    // fetched once per cluster (TMA multicast); needs every group complete
+    // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
+    // Measured with split K / V gather warps (128k Llama): clusters of 2 /
+    // 4 -> K3 16.3-16.4 / 17.1-17.3 ms (4-CTA clusters co-schedule on only
+    // 132 of 148 SMs); AA_K3_CLUSTER overrides.
     if (MODE == SPARSE && !P.lsu && P.T_m % P.step == 0) {
-        for (int c : {AA_CLUSTER_MAX, 2})
-            if (ipg % c == 0) {
+        int want = 2;
+        if (const char* env = getenv("AA_K3_CLUSTER")) want = atoi(env);
+        for (int c : {want, 2, 1})
+            if (c >= 1 && c <= 8 && ipg % c == 0) {
                 P.cluster = c;
                 break;
             }
