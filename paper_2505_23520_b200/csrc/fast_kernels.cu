@@ -94,7 +94,7 @@ constexpr int kPolyPairs = AA_POLY_PAIRS;
 // 8 prologue (to the first S), 9 CTAs, 10 producer wait-empty, 11/12
 // softmax-B wait-S / compute.
 #ifdef AA_PROF
-__device__ unsigned long long g_prof[16];
+__device__ unsigned long long g_prof[6][16];  // [fa_pair MODE | 5 = K2 identify][slot]
 #define PROF(...) __VA_ARGS__
 #else
 #define PROF(...)
@@ -162,6 +162,7 @@ struct PairSmem {
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
     float red[2][2][4];
+    float row_scale[2][kB];  // K3 epilogue: per-row weight of K1's state
 };
 
 __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     const int kt = kv_tile_of(MODE, it, wsb);
                     PROF(const long long t0 = clock64();)
                     if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
-                    PROF(atomicAdd(&g_prof[10], clock64() - t0);)
+                    PROF(atomicAdd(&g_prof[MODE][10], clock64() - t0);)
                     mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
                     tma_load_3d(S.k[sk], &tmK, &S.bar_k_full[sk], 0, kt * kB, kvh);
                     tma_load_3d(S.k[sk] + kAtomBytes, &tmK, &S.bar_k_full[sk], 64, kt * kB, kvh);
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_k_empty[jl % kKStages], (jl / kKStages) & 1);
                 mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
             }
-            PROF(atomicAdd(&g_prof[3], pw_p); atomicAdd(&g_prof[4], pw_k); atomicAdd(&g_prof[5], pw_v);)
+            PROF(atomicAdd(&g_prof[MODE][3], pw_p); atomicAdd(&g_prof[MODE][4], pw_k); atomicAdd(&g_prof[MODE][5], pw_v);)
         }
         __syncwarp();
     } else if (warp < 4) {
@@ -842,7 +843,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     const float mx2 = mx * c;
                     const bool redo = mx2 > m_used + 8.f;
                     if (__any_sync(0xffffffffu, redo)) {  // tcgen05.ld/st are warp-collective
-                        PROF(if (lane == 0 && warp == 4) atomicAdd(&g_prof[13], 1ull);)
                         const float alpha = redo ? ex2(m_used - mx2) : 1.f;
                         if (redo) m_used = mx2;
                         l = l * alpha + emit(m_used);
@@ -879,10 +879,38 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         P.row_stats[static_cast<size_t>(h) * P.n + row] = make_float2(m_used, l);
                 }
             } else {
+            // K3 with the f16 hand-off: K1's state for this row (m, l and the
+            // 256-B acc / l row) is loaded before waiting for the last PV, all
+            // in flight at once, instead of chunk by chunk behind each TMEM read
+            float pre_m = 0.f, pre_l = 1.f;
+            const bool prefetch = MODE == SPARSE && P.acc_f16;
+            // ... and the acc / l tile in the coalesced order of the staged
+            // pass below (thread r: 8 B at float4 slot i*128 + r of each half)
+            uint2 pre_a[2][16];
+            if (prefetch) {
+                if (row < P.n) {
+                    const size_t ri = static_cast<size_t>(h) * P.n + row;
+                    pre_m = P.m_in[ri];
+                    pre_l = P.l_in[ri];
+                }
+                const int rows_v = min(kB, P.n - qx * kB);
+                const __half* acc_h = reinterpret_cast<const __half*>(P.acc_in) +
+                                      (static_cast<size_t>(h) * P.n + qx * kB) * kD;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int rr = (i * kB + r) >> 4;
+                        pre_a[hf][i] = rr < rows_v ? *reinterpret_cast<const uint2*>(
+                                                         acc_h + static_cast<size_t>(rr) * kD + hf * 64 + (r & 15) * 4)
+                                                   : make_uint2(0u, 0u);
+                    }
+            }
             if (nX > 0) {
                 mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
                 tc_fence_after();
             }
+            PROF(if (lane == 0 && warp == 4) atomicAdd(&g_prof[MODE][13], clock64() - t_epi0);)
             if constexpr (MODE == ANCHOR) {
                 // acc_out = O * f (the state rescaled to the true max) leaves
                 // through shared memory so that the global stores are coalesced
@@ -948,6 +976,71 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     P.msum[static_cast<size_t>(h) * P.T_m + qx] =
                         static_cast<double>(S.red[X][0][0]) + S.red[X][0][1] + S.red[X][0][2] + S.red[X][0][3];
                 }
+            } else if (MODE == SPARSE && P.acc_f16) {
+                // merge with K1's state (f16 acc / l hand-off) and leave through
+                // shared memory so that loads and stores are coalesced:
+                //   out = O * (fs * inv) + acc_n * (la * fa * inv)
+                // the first term is staged per row (TMEM lane = row), the second
+                // added in the coalesced pass (row scalar from shared memory)
+                const bool valid_row = row < P.n;
+                const float ma2 = pre_m * kLog2e;
+                const float M = fmaxf(ma2, m_used);
+                const float fa = ex2(ma2 - M);
+                const float fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
+                const float inv = 1.f / (pre_l * fa + l * fs);
+                const float so = fs * inv;
+                S.row_scale[X][r] = valid_row ? pre_l * fa * inv : 0.f;
+                float* stg = reinterpret_cast<float*>(S.q[X]);
+                const int rows_valid = min(kB, P.n - qx * kB);
+                const size_t gbase = (static_cast<size_t>(h) * P.n + qx * kB) * kD;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    if (half) named_bar_sync(1 + X, 128);  // half 0 drained from the staging buffer
+                    uint32_t v[64];
+                    if (nX > 0) {
+                        tmem_ld32(tO + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                        tmem_ld32(tO + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 64; ++jj) v[jj] = 0u;
+                    }
+#pragma unroll
+                    for (int ch = 0; ch < 16; ++ch)
+                        *reinterpret_cast<float4*>(stg + r * 64 + ((ch ^ (r & 15)) << 2)) = make_float4(
+                            __uint_as_float(v[4 * ch]) * so, __uint_as_float(v[4 * ch + 1]) * so,
+                            __uint_as_float(v[4 * ch + 2]) * so, __uint_as_float(v[4 * ch + 3]) * so);
+                    named_bar_sync(1 + X, 128);
+                    PROF(if (half == 0 && lane == 0 && warp == 4) atomicAdd(&g_prof[MODE][14], clock64() - t_epi0);)
+                    // thread r covers float4 i*128 + r (row idx/16, chunk idx%16)
+                    const int ch = r & 15;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int rr = (i * kB + r) >> 4;
+                        if (rr >= rows_valid) continue;
+                        float4 o = *reinterpret_cast<const float4*>(stg + rr * 64 + ((ch ^ (rr & 15)) << 2));
+                        const float sa = S.row_scale[X][rr];
+                        const uint2 a4 = pre_a[half][i];
+                        const float2 a01 = __half22float2(*reinterpret_cast<const __half2*>(&a4.x));
+                        const float2 a23 = __half22float2(*reinterpret_cast<const __half2*>(&a4.y));
+                        o.x += a01.x * sa;
+                        o.y += a01.y * sa;
+                        o.z += a23.x * sa;
+                        o.w += a23.y * sa;
+                        const size_t ge = gbase + static_cast<size_t>(rr) * kD + half * 64 + ch * 4;
+                        if (P.out_bf16) {
+                            __nv_bfloat162 t0 = __floats2bfloat162_rn(o.x, o.y);
+                            __nv_bfloat162 t1 = __floats2bfloat162_rn(o.z, o.w);
+                            uint2 w;
+                            w.x = *reinterpret_cast<uint32_t*>(&t0);
+                            w.y = *reinterpret_cast<uint32_t*>(&t1);
+                            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(P.out) + ge) = w;
+                        } else {
+                            *reinterpret_cast<float4*>(static_cast<float*>(P.out) + ge) = o;
+                        }
+                    }
+                    PROF(if (half == 0 && lane == 0 && warp == 4) atomicAdd(&g_prof[MODE][15], clock64() - t_epi0);)
+                }
             } else {
             const bool valid_row = row < P.n;
             const size_t rowoff = (static_cast<size_t>(h) * P.n + (valid_row ? row : 0)) * kD;
@@ -962,7 +1055,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
                     inv = 1.f / (la * fa + l * fs);
                     acc_a = P.acc_in + rowoff;
-                    if (P.acc_f16) fa *= la;  // acc_in holds acc / l
                 } else {
                     inv = 1.f / l;
                 }
@@ -980,20 +1072,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         float o[32];
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) o[jj] = __uint_as_float(v[jj]) * fs;
-                        if (MODE == SPARSE && P.acc_f16) {
-                            const __half* ah = reinterpret_cast<const __half*>(P.acc_in) + rowoff + ch * 32;
-#pragma unroll
-                            for (int jj = 0; jj < 32; jj += 8) {
-                                const uint4 raw = *reinterpret_cast<const uint4*>(ah + jj);
-                                const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const float2 a = __half22float2(h2[u]);
-                                    o[jj + 2 * u] += a.x * fa;
-                                    o[jj + 2 * u + 1] += a.y * fa;
-                                }
-                            }
-                        } else if (MODE == SPARSE) {
+                        if (MODE == SPARSE) {
 #pragma unroll
                             for (int jj = 0; jj < 32; jj += 4) {
                                 const float4 a = *reinterpret_cast<const float4*>(acc_a + ch * 32 + jj);
@@ -1032,12 +1111,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }  // MODE != RECALL
             PROF(if (lane == 0 && (warp == 4 || warp == 8)) {
                 const int o = warp == 4 ? 0 : 11;
-                atomicAdd(&g_prof[o], ps_wait);
-                atomicAdd(&g_prof[o + 1], ps_comp);
+                atomicAdd(&g_prof[MODE][o], ps_wait);
+                atomicAdd(&g_prof[MODE][o + 1], ps_comp);
                 if (warp == 4) {
-                    atomicAdd(&g_prof[2], static_cast<unsigned long long>(nX));
-                    atomicAdd(&g_prof[7], clock64() - t_epi0);
-                    if (nX > 0) atomicAdd(&g_prof[8], ps_first - t_cta0);
+                    atomicAdd(&g_prof[MODE][2], static_cast<unsigned long long>(nX));
+                    atomicAdd(&g_prof[MODE][7], clock64() - t_epi0);
+                    if (nX > 0) atomicAdd(&g_prof[MODE][8], ps_first - t_cta0);
                 }
             })
         }
@@ -1048,8 +1127,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
     PROF(if (threadIdx.x == 0) {
-        atomicAdd(&g_prof[6], clock64() - t_cta0);
-        atomicAdd(&g_prof[9], 1ull);
+        atomicAdd(&g_prof[MODE][6], clock64() - t_cta0);
+        atomicAdd(&g_prof[MODE][9], 1ull);
     })
 }
 
@@ -1162,7 +1241,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                     const int b = nk % kIdStages;
                     PROF(const long long t0 = clock64();)
                     if (nk >= kIdStages) mbar_wait(&S.bar_k_empty[b], ((nk / kIdStages) - 1) & 1);
-                    PROF(atomicAdd(&g_prof[0], clock64() - t0);)
+                    PROF(atomicAdd(&g_prof[5][0], clock64() - t0);)
                     mbar_expect_tx(&S.bar_k_full[b], kTileBytes);
                     const int key0 = static_cast<int>(w.geo.b_kv) + t * kB;
                     tma_load_3d(S.k[b], &tmK, &S.bar_k_full[b], 0, key0, kvh);
@@ -1186,7 +1265,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                     const int b = nk % kIdStages;
                     PROF(const long long t0 = clock64();)
                     mbar_wait(&S.bar_k_full[b], (nk / kIdStages) & 1);
-                    PROF(atomicAdd(&g_prof[1], clock64() - t0); atomicAdd(&g_prof[9], 1ull);)
+                    PROF(atomicAdd(&g_prof[5][1], clock64() - t0); atomicAdd(&g_prof[5][9], 1ull);)
                     const uint32_t lk = lk0 + b * (kTileBytes >> 4);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
@@ -1194,7 +1273,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                         const int sb = ns[m] & 1;
                         PROF(const long long t0 = clock64();)
                         if (ns[m] >= 2) mbar_wait(&S.bar_s_empty[m][sb], ((ns[m] >> 1) - 1) & 1);
-                        PROF(atomicAdd(&g_prof[2], clock64() - t0);)
+                        PROF(atomicAdd(&g_prof[5][2], clock64() - t0);)
                         tc_fence_after();
                         const uint32_t lhi = la0 + m * (2 * kTileBytes >> 4), llo = lhi + (kTileBytes >> 4);
                         const uint32_t d_tmem = tmem + (2 * m + sb) * 128;
@@ -1243,7 +1322,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                 const int sb = ns & 1;
                 PROF(const long long t0 = clock64();)
                 mbar_wait(&S.bar_s_full[m][sb], (ns >> 1) & 1);
-                PROF(const long long t1 = clock64(); if (lane == 0 && (warp == 2 || warp == 6)) atomicAdd(&g_prof[3], t1 - t0);)
+                PROF(const long long t1 = clock64(); if (lane == 0 && (warp == 2 || warp == 6)) atomicAdd(&g_prof[5][3], t1 - t0);)
                 tc_fence_after();
                 const int64_t key0 = w.geo.b_kv + static_cast<int64_t>(t) * kB;
                 uint32_t wd[4];
@@ -1278,7 +1357,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                     const int64_t word0 = (key0 - w.geo.b_kv) >> 5;
                     *reinterpret_cast<uint4*>(rowbits + word0) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
                 }
-                PROF(if (lane == 0 && (warp == 2 || warp == 6)) { atomicAdd(&g_prof[4], clock64() - t1); atomicAdd(&g_prof[5], 1ull); })
+                PROF(if (lane == 0 && (warp == 2 || warp == 6)) { atomicAdd(&g_prof[5][4], clock64() - t1); atomicAdd(&g_prof[5][5], 1ull); })
             }
         }
     }
@@ -1286,7 +1365,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
     __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
-    PROF(if (threadIdx.x == 0) { atomicAdd(&g_prof[6], clock64() - t_cta0); atomicAdd(&g_prof[7], 1ull); })
+    PROF(if (threadIdx.x == 0) { atomicAdd(&g_prof[5][6], clock64() - t_cta0); atomicAdd(&g_prof[5][7], 1ull); })
 }
 
 // q_bar (f32 [hq, G, d]) -> A operand rows r = g*rep + hh of KV head kvh as a
@@ -1751,9 +1830,9 @@ cudaError_t fast_tile_mass(const FastArgs& f, const void* q, const void* k, floa
 #ifdef AA_PROF
 extern "C" int aa_prof_read(unsigned long long* out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, aa::g_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, aa::g_prof, sizeof(unsigned long long) * 96) != cudaSuccess) return -1;
     if (reset) {
-        static const unsigned long long z[16] = {};
+        static const unsigned long long z[96] = {};
         if (cudaMemcpyToSymbol(aa::g_prof, z, sizeof(z)) != cudaSuccess) return -1;
     }
     return 0;

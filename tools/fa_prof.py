@@ -56,11 +56,9 @@ def main():
 
     L = capi.lib()
     L.aa_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-    buf = (C.c_ulonglong * 16)()
+    buf = (C.c_ulonglong * 96)()
 
-    def read(name):
-        assert L.aa_prof_read(buf, 1) == 0
-        v = list(buf)
+    def report(name, v):
         ctas = max(1, v[9])
         tiles = max(1, v[2])
         row = {"kernel": name, "ctas": v[9], "tiles_per_cta_A": v[2] / ctas}
@@ -69,7 +67,9 @@ def main():
                 continue
             row[s + "_per_cta"] = round(v[i] / ctas)
         row["smA_compute_per_tile"] = round(v[1] / tiles)
-        row["redo_per_tile_warp4"] = round(v[13] / tiles, 4)
+        row["epi_wait_odone_per_cta"] = round(v[13] / ctas)
+        row["epi_t_staged0"] = round(v[14] / ctas)
+        row["epi_t_half0_done"] = round(v[15] / ctas)
 
         row["smA_wait_per_tile"] = round(v[0] / tiles)
         row["lib"] = os.path.basename(a.lib)
@@ -84,21 +84,25 @@ def main():
         qs.append(q), ks.append(k), vs.append(v)
     q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
     cfg = capi.BlockConfig(128, 128, 16, 12.0)
+    pipe = capi.Pipeline(q, k, v, cfg)
+    out = torch.empty((a.hq, a.n, 128), dtype=torch.float32, device=dev)
     for rnd in range(2):
+        # the fused chain (f16 hand-off, the bench path): K1 and K3 rows
         L.aa_prof_read(buf, 1)
-        st = capi.compute_anchor(q, k, v, cfg)
-        read("k1_anchor")
-        anchor, qbar = capi.pool(q, k, st, cfg)
-        idx, counts = capi.identify(q, k, qbar, anchor, cfg)
-        L.aa_prof_read(buf, 1)
-        out, comp = capi.sparse(q, k, v, st, idx, counts, cfg)
-        read("k3_sparse " + os.environ.get("AA_K3_GATHER", "tma"))
-        del st, out
+        pipe(q, k, v, out=out)
+        torch.cuda.synchronize()
+        assert L.aa_prof_read(buf, 1) == 0
+        allv = list(buf)
+        for name, mode in (("k1_anchor", 0), ("k3_sparse " + os.environ.get("AA_K3_GATHER", "tma"), 1)):
+            report(name, allv[16 * mode:16 * mode + 16])
         if not a.no_dense and rnd == 0:
             nd = min(a.n, 32768)
+            L.aa_prof_read(buf, 1)
             capi.dense_attention(q[:, :nd].contiguous(), k[:, :nd].contiguous(),
                                  v[:, :nd].contiguous(), out_dtype=torch.bfloat16)
-            read(f"dense n={nd}")
+            torch.cuda.synchronize()
+            assert L.aa_prof_read(buf, 1) == 0
+            report(f"dense n={nd}", list(buf)[32:48])
 
 
 if __name__ == "__main__":
