@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     } else if (warp == 1) {
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
-        if (!kTileIssue && lane == 0 && ntiles > 0) {
+        if (!kTileIssue && ntiles > 0) {  // the whole warp; one elected lane issues
             // SW128 descriptors: the high word (SBO 1024, version, layout) is a
             // constant, the low word = start address >> 4 | LBO >> 4 << 16
             constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
@@ -443,10 +443,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
-                    mma_ss(tmem + X * 128, kDescHi | (lq + off), kDescHi | (lk + off), kIdescQK,
+                    mma_ss_w(tmem + X * 128, kDescHi | (lq + off), kDescHi | (lk + off), kIdescQK,
                            kk > 0 ? 1u : 0u);
                 }
-                mma_commit(&S.bar_s_full[X]);
+                mma_commit_w(&S.bar_s_full[X]);
             };
             auto pv = [&](int X, int j) {
                 const int st = j & 1;
@@ -462,13 +462,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
+                    mma_ts_w(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
                            (j > 0 || kk > 0) ? 1u : 0u);
-                mma_commit(&S.bar_o_done[X]);
+                mma_commit_w(&S.bar_o_done[X]);
             };
             // a stage is released to every producer of the cluster that fills it
             auto release = [&](uint64_t* bar) {
-                if (C > 1) mma_commit_mc(bar, cmask); else mma_commit(bar);
+                if (C > 1) mma_commit_mc_w(bar, cmask); else mma_commit_w(bar);
             };
             mbar_wait(&S.bar_q, 0);
             if (nA > 0) qk(0, 0);
