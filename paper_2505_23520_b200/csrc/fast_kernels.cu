@@ -80,13 +80,17 @@ constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K
 constexpr uint32_t kIdescPV = idesc_f16(0, 0, 1, 128, 128);  // f16 x f16,  B MN-major
 constexpr float kLog2e = 1.4426950408889634f;
 // Exp2 pairs per 32 columns computed by ex2_poly2 on the FMA pipe instead of
-// MUFU.  Measured on B200 (128k Llama layer, profiles/README.md): 0 / 4 / 6 /
-// 8 pairs -> K3 18.6 / 19.2 / 19.5 / 20.0 ms — the softmax is issue-bound,
-// not MUFU-bound, so the offload is off.
+// MUFU (16 results / clock / SM on B200: one 128 x 128 tile costs >= 1100
+// MUFU cycles per warp, as much as the tile's MMAs).  Measured per kernel
+// (128k Llama, elect-issued MMAs): K1 0 / 2 / 4 pairs -> 3.47 / 3.28-3.33 /
+// 3.26-3.28 ms; K3 0 / 2 / 4 -> 16.3 / 16.8-17.1 / 16.8-16.9 ms (the heavier
+// softmax stream slows the MMA hand-off there).  So K1 offloads 4 of 16.
 #ifndef AA_POLY_PAIRS
 #define AA_POLY_PAIRS 0
 #endif
-constexpr int kPolyPairs = AA_POLY_PAIRS;
+#ifndef AA_POLY_PAIRS_K1
+#define AA_POLY_PAIRS_K1 4
+#endif
 
 // Optional cycle accounting of the fa_pair roles (build with -DAA_PROF; read
 // through aa_prof_read).  Slots: 0/1 softmax-A wait-S / compute, 2 softmax-A
@@ -729,7 +733,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         const float2 x = ffma2(make_float2(__uint_as_float(v[ch * 32 + jj]),
                                                            __uint_as_float(v[ch * 32 + jj + 1])),
                                                c, -base);
-                        const float2 pp = (jj >> 1) % 16 < kPolyPairs ? ex2_poly2(x)
+                        const float2 pp = (jj >> 1) % 16 < (MODE == ANCHOR ? AA_POLY_PAIRS_K1 : AA_POLY_PAIRS)
+                                              ? ex2_poly2(x)
                                                                       : make_float2(ex2(x.x), ex2(x.y));
                         lsum = fadd2(lsum, pp);
                         pk[jj >> 1] = pack_half2(pp.x, pp.y);
