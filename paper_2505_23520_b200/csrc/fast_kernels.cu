@@ -8,8 +8,9 @@
 //   D  dense    fa_pair<DENSE>   tiles 0..qb (causal baseline)
 //
 // fa_pair (see its comment): one CTA = two 128-row query blocks of one head
-// sharing every K/V tile; TMA producer warp, single-thread tcgen05 issuer,
-// two softmax warpgroups ping-ponging on the tensor pipe; S/P/O in TMEM.
+// sharing every K/V tile; TMA producer warp(s), one MMA warp issuing
+// tcgen05.mma from an elected lane, two softmax warpgroups ping-ponging on the
+// tensor pipe; S/P/O in TMEM.
 // Softmax is exp2-based with lazy rescaling (O/l rescaled only when the
 // running max grows by > 8 in log2 units); the state written out is exact
 // (rescaled to the true max).  PV runs in f16 (P in [0, 256] keeps 11
@@ -38,42 +39,12 @@ using namespace sm100;
 constexpr int kB = 128;  // b_q = b_kv
 constexpr int kD = 128;  // head dim
 constexpr int kPairThreads = 384;   // fa_pair CTA
-constexpr int kLsuThreads = 64;     // K3 lsu mode: warps 2-3 gather the stripe rows
 // K ring depth of fa_pair (V keeps 2 stages): K(j + kKStages) can be fetched as
 // soon as QK_B(j) has read stage j — one more tile of lead for the gathers.
 #ifndef AA_K_STAGES
 #define AA_K_STAGES 2
 #endif
 constexpr int kKStages = AA_K_STAGES;
-// Each query tile's softmax warpgroup issues its own MMAs (PV_X(j), QK_X(j+1))
-// right after a named barrier over its 128 threads, instead of handing P to a
-// separate MMA warp through an mbarrier (no wake-up hop, no coupling of the
-// two tiles' MMA streams through one issuing thread).
-#ifndef AA_TILE_ISSUE
-#define AA_TILE_ISSUE 0
-#endif
-constexpr bool kTileIssue = AA_TILE_ISSUE != 0;
-// The two tiles' softmax sections strictly alternate (named-barrier tokens,
-// FA4-style): while one tile computes exponentials the tensor pipe works on
-// the other tile's PV / QK, and the two never contend for MUFU.
-#ifndef AA_PINGPONG
-#define AA_PINGPONG 0
-#endif
-constexpr bool kPingPong = AA_PINGPONG != 0;
-// K3 (TMA gathers): K rows are gathered by warp 0 and V rows by warp 3, each
-// at its own pace, instead of one loop that blocks on V's free stage before
-// it can fetch the next K tile.
-#ifndef AA_KV_SPLIT
-#define AA_KV_SPLIT 1
-#endif
-constexpr bool kKvSplit = AA_KV_SPLIT != 0;
-// The same split for the contiguous K/V tiles of K1 / dense (V loads on warp 3,
-// K1's column sums on warp 2 alone): measured neutral-to-negative (K1 +2%),
-// off.
-#ifndef AA_KV_SPLIT_TILES
-#define AA_KV_SPLIT_TILES 0
-#endif
-constexpr bool kKvSplitTiles = AA_KV_SPLIT_TILES != 0;
 constexpr uint32_t kTileBytes = kB * kD * 2;   // 32 KB (bf16 / f16 tile)
 constexpr uint32_t kAtomBytes = kB * 64 * 2;   // 16 KB: 128 rows x 128 B (SW128 atom column)
 constexpr uint32_t kIdescQK = idesc_f16(1, 1, 0, 128, 128);  // bf16 x bf16, B K-major
@@ -140,13 +111,10 @@ struct FaParams {
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
     int item0;    // first work item of this launch (K3 split launches)
-    int lsu;      // K3: gather the stripe rows with cp.async (warps 2-3) instead of TMA gather4
     // K1 -> K3 hand-off format: 0 = acc f32 unnormalised (AnchorState::acc,
     // the stage API); 1 = f16 acc / l (normalised, |.| <= max|v|: half the
     // bytes both ways; the fused chain)
     int acc_f16;
-    const uint8_t* k_rows;    // K base (rows of d bf16, 256 B) for the LSU gathers
-    const uint8_t* v16_rows;  // packed f16 V [hkv, n, d]
     // RECALL inputs / output
     const uint32_t* bits;   // selection bitmask [hq, G, words_per_row]
     int64_t words_per_row;
@@ -177,8 +145,11 @@ __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
 // One CTA = two query blocks (A = qb, B = qb + 1) of one head and one group;
 // they share every K/V tile (and for K3 the same gathered stripe rows), so
 // each tile is loaded once for 256 query rows.  12 warps:
-//   warp 0      TMA producer (Q pair once; K and V through 2-stage rings)
-//   warp 1      TMEM allocator (512 columns) + single-thread MMA issuer
+//   warp 0      TMA producer (Q pair once; K and V through 2-stage rings;
+//               in K3 the K-row gathers only)
+//   warp 1      TMEM allocator (512 columns) + MMA issuer (the whole warp runs
+//               the loop with warp-uniform operands, one elected lane issues)
+//   warps 2-3   K1: pooled column sums of Q; K3: warp 3 gathers the V rows
 //   warps 4-7   softmax / epilogue of query tile A   (TMEM lanes 0..127)
 //   warps 8-11  softmax / epilogue of query tile B
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512); P_X is written
@@ -243,18 +214,14 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
-        mbar_init(&S.bar_qsum, kKvSplitTiles ? 32 : 64);
-        const uint32_t fills = (MODE == SPARSE && P.lsu) ? kLsuThreads : 1;
-        // with per-tile issue, each tile's issuer releases every stage once
-        // (twice when the other tile does not use it)
-        const uint32_t releases = (kTileIssue ? 2 : 1) * C;
+        mbar_init(&S.bar_qsum, 64);
         for (int b = 0; b < kKStages; ++b) {
-            mbar_init(&S.bar_k_full[b], fills);
-            mbar_init(&S.bar_k_empty[b], releases);
+            mbar_init(&S.bar_k_full[b], 1);
+            mbar_init(&S.bar_k_empty[b], C);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&S.bar_v_full[b], fills);
-            mbar_init(&S.bar_v_empty[b], releases);
+            mbar_init(&S.bar_v_full[b], 1);
+            mbar_init(&S.bar_v_empty[b], C);
             mbar_init(&S.bar_s_full[b], 1);
             mbar_init(&S.bar_p_full[b], 128);
             mbar_init(&S.bar_o_done[b], 1);
@@ -323,83 +290,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
             }
         }
-#ifdef AA_K3_ACC_PREFETCH
-        if (MODE == SPARSE && lane == 0 && ntiles > 0) {
-            // the epilogue's K1 state rows (acc: 64 KB per query tile) -> L2 now
-            // (measured: no epilogue gain, +0.9 GB of K/V gather re-reads)
-            for (int X = 0; X < (hasB ? 2 : 1); ++X) {
-                const int r0 = (X ? qB : qA) * kB;
-                const int rows = min(kB, P.n - r0);
-                bulk_prefetch_l2(P.acc_in + (static_cast<size_t>(h) * P.n + r0) * kD,
-                                 static_cast<uint32_t>(rows) * kD * 4);
-            }
-        }
-#endif
-        if (MODE == SPARSE && !P.lsu && kKvSplit) {
-            gather_split(true);
-        } else if (MODE == SPARSE && !P.lsu) {
-            // Gather lanes: each issues gather4 for 4 of the tile's rows (x 2
-            // column halves, for K and for V).  Standalone CTA: 32 lanes cover
-            // the 128 rows; in a cluster of C, this CTA covers rows
-            // [crank*128/C, (crank+1)*128/C) and multicasts them.
-            const int lanes = 32 / C;
-            const bool gl = lane < lanes;
-            const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
-            auto fetch = [&](int t, int (&j)[4]) {
-                const int base = t * kB;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = base + row0 + u;
-                    j[u] = gl ? static_cast<int>(list[e < count ? e : base]) : 0;
-                }
-            };
-            int j[4];
-            if (ntiles > 0) fetch(0, j);
-            const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
-            for (int it = 0; it < ntiles; ++it) {
-                const int st = it & 1;
-                const int sk = it % kKStages;
-                int rk[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) rk[u] = kvh * P.kv_head_rows + j[u] * P.kv_row_rows;
-                if (lane == 0) {
-                    if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
-                    mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
-                }
-                __syncwarp();
-                uint8_t* kd = S.k[sk] + row0 * 128;
-                if (gl) {
-                    if (C > 1) {
-                        tma_gather4_mc(kd, &tmKg, &S.bar_k_full[sk], cmask, 0, rk[0], rk[1], rk[2], rk[3]);
-                        tma_gather4_mc(kd + kAtomBytes, &tmKg, &S.bar_k_full[sk], cmask, 64, rk[0], rk[1],
-                                       rk[2], rk[3]);
-                    } else {
-                        tma_gather4(kd, &tmKg, &S.bar_k_full[sk], 0, rk[0], rk[1], rk[2], rk[3]);
-                        tma_gather4(kd + kAtomBytes, &tmKg, &S.bar_k_full[sk], 64, rk[0], rk[1], rk[2],
-                                    rk[3]);
-                    }
-                }
-                if (lane == 0) {
-                    if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
-                    mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
-                }
-                __syncwarp();
-                uint8_t* vd = S.v[st] + row0 * 128;
-                if (gl) {
-                    if (C > 1) {
-                        tma_gather4_mc(vd, &tmVg, &S.bar_v_full[st], cmask, 0, vh + j[0], vh + j[1],
-                                       vh + j[2], vh + j[3]);
-                        tma_gather4_mc(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], cmask, 64, vh + j[0],
-                                       vh + j[1], vh + j[2], vh + j[3]);
-                    } else {
-                        tma_gather4(vd, &tmVg, &S.bar_v_full[st], 0, vh + j[0], vh + j[1], vh + j[2],
-                                    vh + j[3]);
-                        tma_gather4(vd + kAtomBytes, &tmVg, &S.bar_v_full[st], 64, vh + j[0], vh + j[1],
-                                    vh + j[2], vh + j[3]);
-                    }
-                }
-                if (it + 1 < ntiles) fetch(it + 1, j);
-            }
+        if (MODE == SPARSE) {
+            gather_split(true);  // V rows: warp 3
         } else if (MODE != SPARSE) {
             for (int it = 0; it < ntiles; ++it) {
                 if (lane == 0) {
@@ -412,7 +304,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     mbar_expect_tx(&S.bar_k_full[sk], kTileBytes);
                     tma_load_3d(S.k[sk], &tmK, &S.bar_k_full[sk], 0, kt * kB, kvh);
                     tma_load_3d(S.k[sk] + kAtomBytes, &tmK, &S.bar_k_full[sk], 64, kt * kB, kvh);
-                    if (!kQkOnly<MODE> && !kKvSplitTiles) {
+                    if (!kQkOnly<MODE>) {
                         if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
                         mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
                         tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
@@ -425,7 +317,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     } else if (warp == 1) {
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ MMA issuer
-        if (!kTileIssue && ntiles > 0) {  // the whole warp; one elected lane issues
+        if (ntiles > 0) {  // the whole warp runs the loop; one elected lane issues
             // SW128 descriptors: the high word (SBO 1024, version, layout) is a
             // constant, the low word = start address >> 4 | LBO >> 4 << 16
             constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
@@ -440,7 +332,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_k_full[st], (j / kKStages) & 1);
                 PROF(pw_k += clock64() - t0;)
                 tc_fence_after();
-                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
                 // descriptors are built once; the k-step only moves the start
                 // address field (addr >> 4, no carry below 256 KB)
                 const uint32_t lq = X ? lq1 : lq0, lk = lk0 + st * (kTileBytes >> 4);
@@ -461,7 +352,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
                 PROF(pw_v += clock64() - t1;)
                 tc_fence_after();
-                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
                 const uint32_t lv = lv0 + st * (kTileBytes >> 4);
                 const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * 128;
 #pragma unroll
@@ -501,110 +391,31 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         }
         __syncwarp();
     } else if (warp < 4) {
-        setmaxnreg_dec<56>();  // warps 2-3: LSU gathers of K3 (lsu mode), K1 column sums
-        if (MODE == SPARSE && !P.lsu && kKvSplit && warp == 3) gather_split(false);
-        if (MODE != SPARSE && !kQkOnly<MODE> && kKvSplitTiles && warp == 3 && lane == 0) {
-            // V tiles at their own pace (the K tiles come from warp 0)
-            for (int it = 0; it < ntiles; ++it) {
-                const int st = it & 1;
-                const int kt = kv_tile_of(MODE, it, wsb);
-                if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
-                mbar_expect_tx(&S.bar_v_full[st], kTileBytes);
-                tma_load_3d(S.v[st], &tmV, &S.bar_v_full[st], 0, kt * kB, kvh);
-                tma_load_3d(S.v[st] + kAtomBytes, &tmV, &S.bar_v_full[st], 64, kt * kB, kvh);
-            }
-        }
-        if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0 && (warp == 2 || !kKvSplitTiles)) {
+        setmaxnreg_dec<56>();  // warp 3: K3's V-row gathers; warps 2-3: K1's column sums
+        if (MODE == SPARSE && warp == 3) gather_split(false);
+        if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
             // pooled-query partials (avgpool_rows, R/src/matrix.cpp:44-65): column
             // sums of each query tile over its 128 rows (TMA zero-fills rows past
-            // n), summed in row order; each thread owns column pairs (2 pairs on
-            // warp 2 alone when warp 3 loads V).  Runs beside the main loop, off
-            // the epilogue's critical path.
+            // n), summed in row order; thread t owns columns 2t, 2t+1.  Runs
+            // beside the main loop, off the epilogue's critical path.
             const int t = threadIdx.x - 64;
-            constexpr int kPairsPerThread = kKvSplitTiles ? 2 : 1;
+            const int col = 2 * t;
+            const int chunk = (col & 63) >> 3, e = col & 7;
             mbar_wait(&S.bar_q, 0);
             for (int X = 0; X < (hasB ? 2 : 1); ++X) {
-#pragma unroll
-                for (int pp = 0; pp < kPairsPerThread; ++pp) {
-                    const int col = 2 * (t * kPairsPerThread + pp);
-                    const int chunk = (col & 63) >> 3, e = col & 7;
-                    const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes + e * 2;
-                    float s0 = 0.f, s1 = 0.f;
+                const uint8_t* atom = S.q[X] + (col >> 6) * kAtomBytes + e * 2;
+                float s0 = 0.f, s1 = 0.f;
 #pragma unroll 16
-                    for (int rr = 0; rr < kB; ++rr) {
-                        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(
-                            atom + rr * 128 + ((chunk ^ (rr & 7)) << 4));
-                        s0 += __low2float(x);
-                        s1 += __high2float(x);
-                    }
-                    *reinterpret_cast<float2*>(P.qsum + (static_cast<size_t>(h) * P.T_m + (X ? qB : qA)) * kD +
-                                               col) = make_float2(s0, s1);
+                for (int rr = 0; rr < kB; ++rr) {
+                    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(
+                        atom + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+                    s0 += __low2float(x);
+                    s1 += __high2float(x);
                 }
+                *reinterpret_cast<float2*>(P.qsum + (static_cast<size_t>(h) * P.T_m + (X ? qB : qA)) * kD + col) =
+                    make_float2(s0, s1);
             }
             mbar_arrive(&S.bar_qsum);  // the epilogue reuses the Q tiles as staging
-        }
-        if (MODE == SPARSE && P.lsu) {
-            // Warp w in {2, 3} fills rows [64 (w - 2), 64 (w - 2) + 64) of every K
-            // and V tile; half-warp h copies row 2i + h, 16 lanes x 16 B = one
-            // 256-B row, into the 128B-swizzled K-major atoms TMA would write.
-            // Each thread waits for its own copies, fences them into the async
-            // proxy and arrives (full barriers count kLsuThreads arrivals).
-            const int wr = (warp - 2) * 64;
-            const int hsel = lane >> 4, sub = lane & 15;
-            const uint32_t chunk_off = static_cast<uint32_t>((sub >> 3) * kAtomBytes);
-            const int c8 = sub & 7;
-            const uint8_t* kbase = P.k_rows + static_cast<size_t>(kvh) * P.kv_head_rows * 256 + sub * 16;
-            const uint8_t* vbase = P.v16_rows + static_cast<size_t>(kvh) * P.n * 256 + sub * 16;
-            const size_t kstride = static_cast<size_t>(P.kv_row_rows) * 256;
-            for (int it = 0; it < ntiles; ++it) {
-                const int st = it & 1;
-                const int sk = it % kKStages;
-                const int base = it * kB;
-                const int e0 = base + wr + lane, e1 = e0 + 32;
-                const uint32_t a0 = list[e0 < count ? e0 : base];
-                const uint32_t a1 = list[e1 < count ? e1 : base];
-                if (it >= kKStages) mbar_wait(&S.bar_k_empty[sk], ((it / kKStages) - 1) & 1);
-                const uint32_t kd = smem_u32(S.k[sk]) + chunk_off;
-#pragma unroll 8
-                for (int i = 0; i < 32; ++i) {
-                    const int rho = 2 * i + hsel;  // row within this warp's 64
-                    const uint32_t j = __shfl_sync(0xffffffffu, i < 16 ? a0 : a1, rho & 31);
-                    const int r = wr + rho;
-                    cp_async16(kd + r * 128 + ((c8 ^ (r & 7)) << 4), kbase + j * kstride);
-                }
-                if (P.lsu == 2) {
-                    cp_async_arrive_noinc(&S.bar_k_full[sk]);
-                } else {
-                    cp_async_commit();
-                    if (it >= 1) {  // V(it-1) landed
-                        cp_async_wait<1>();
-                        fence_proxy_async_smem();
-                        mbar_arrive(&S.bar_v_full[(it - 1) & 1]);
-                    }
-                }
-                if (it >= 2) mbar_wait(&S.bar_v_empty[st], ((it >> 1) - 1) & 1);
-                const uint32_t vd = smem_u32(S.v[st]) + chunk_off;
-#pragma unroll 8
-                for (int i = 0; i < 32; ++i) {
-                    const int rho = 2 * i + hsel;
-                    const uint32_t j = __shfl_sync(0xffffffffu, i < 16 ? a0 : a1, rho & 31);
-                    const int r = wr + rho;
-                    cp_async16(vd + r * 128 + ((c8 ^ (r & 7)) << 4), vbase + static_cast<size_t>(j) * 256);
-                }
-                if (P.lsu == 2) {
-                    cp_async_arrive_noinc(&S.bar_v_full[st]);
-                } else {
-                    cp_async_commit();
-                    cp_async_wait<1>();  // K(it) landed
-                    fence_proxy_async_smem();
-                    mbar_arrive(&S.bar_k_full[sk]);
-                }
-            }
-            if (ntiles > 0 && P.lsu == 1) {
-                cp_async_wait<0>();
-                fence_proxy_async_smem();
-                mbar_arrive(&S.bar_v_full[(ntiles - 1) & 1]);
-            }
         }
     } else {
         setmaxnreg_inc<224>();
@@ -636,73 +447,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 wstart_x = min(wsbx * kB, P.n);
             }
 
-            // per-tile MMA issue (kTileIssue): lane 0 of the tile's first warp
-            const bool issuer = kTileIssue && quad == 0 && lane == 0;
-            const int nO = X ? nA : nB;  // the other tile's tile count
-            constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
-            const uint32_t lqX = sdesc_sw128_lo(smem_u32(S.q[X]), 16);
-            const uint32_t lk0 = sdesc_sw128_lo(smem_u32(S.k[0]), 16);
-            const uint32_t lv0 = sdesc_sw128_lo(smem_u32(S.v[0]), kAtomBytes);
-            // stage t is released by each tile that uses it (twice by this tile
-            // if the other tile does not), to every producer of the cluster
-            auto release = [&](uint64_t* bar, int t) {
-                const int times = t < nO ? 1 : 2;
-                for (int i = 0; i < times; ++i) {
-                    if (C > 1) mma_commit_mc(bar, cmask); else mma_commit(bar);
-                }
-            };
-            auto issue_qk = [&](int t) {
-                const int st = t % kKStages;
-                mbar_wait(&S.bar_k_full[st], (t / kKStages) & 1);
-                tc_fence_after();
-                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
-                const uint32_t lk = lk0 + st * (kTileBytes >> 4);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
-                    mma_ss(tmem + X * 128, kDescHi | (lqX + off), kDescHi | (lk + off), kIdescQK,
-                           kk > 0 ? 1u : 0u);
-                }
-                mma_commit(&S.bar_s_full[X]);
-                release(&S.bar_k_empty[st], t);
-            };
-            auto issue_pv = [&](int t) {
-                const int st = t & 1;
-                mbar_wait(&S.bar_v_full[st], (t >> 1) & 1);
-                tc_fence_after();
-                if (MODE == SPARSE && P.lsu == 2) fence_proxy_async_smem();
-                const uint32_t lv = lv0 + st * (kTileBytes >> 4);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tmem + 256 + X * 128, tmem + X * 128 + kk * 8, kDescHi | (lv + kk * (2048 >> 4)),
-                           kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
-                mma_commit(&S.bar_o_done[X]);
-                release(&S.bar_v_empty[st], t);
-            };
-            // P(it) is in TMEM (or S(it) consumed): hand the tile to the tensor pipe
-            auto tile_done = [&](int it) {
-                if constexpr (kTileIssue) {
-                    named_bar_sync(1 + X, 128);
-                    if (issuer) {
-                        tc_fence_after();
-                        if (!kQkOnly<MODE>) issue_pv(it);
-                        if (it + 1 < nX) issue_qk(it + 1);
-                        if (it + 1 == nX && C > 1 && X == 0) {
-                            // every CTA's last releases have landed before the exit
-                            // cluster barrier (no remote arrive targets a retired CTA)
-                            const int jl = ntiles - 1;
-                            mbar_wait(&S.bar_k_empty[jl % kKStages], (jl / kKStages) & 1);
-                            mbar_wait(&S.bar_v_empty[jl & 1], (jl >> 1) & 1);
-                        }
-                    }
-                } else {
-                    mbar_arrive(&S.bar_p_full[X]);
-                }
-            };
-            if (issuer && nX > 0) {
-                mbar_wait(&S.bar_q, 0);
-                issue_qk(0);
-            }
             PROF(long long ps_wait = 0, ps_comp = 0, ps_t1 = 0, ps_first = 0;)
             for (int it = 0; it < nX; ++it) {
                 int lim;
@@ -717,11 +461,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_wait(&S.bar_s_full[X], it & 1);
                 PROF(ps_t1 = clock64(); ps_wait += ps_t1 - ps_t0; if (it == 0) ps_first = ps_t1;)
                 tc_fence_after();
-                // ping-pong token: A(it) after B(it-1), B(it) after A(it)
-                if (kPingPong && !kQkOnly<MODE>) {
-                    if (X == 0 ? (it >= 1 && it - 1 < nB) : (it < nA))
-                        named_bar_sync(X == 0 ? 3 : 4, 256);
-                }
                 // single pass: the whole S row in registers
                 uint32_t v[128];
                 // P = 2^(s*c - base) as f16 over S columns [16 ch, 16 ch + 16)
@@ -779,7 +518,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                         rm = (acc2.x + acc2.y) / st.y;
                     }
                     tc_fence_before();
-                    tile_done(it);  // S consumed
+                    mbar_arrive(&S.bar_p_full[X]);  // S consumed
 #pragma unroll
                     for (int sh = 16; sh; sh >>= 1) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
                     if (lane == 0) S.red[X][it & 1][quad] = rm;
@@ -827,7 +566,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     l += la.x + la.y;
                     l_sel += ls.x + ls.y;
                     tc_fence_before();
-                    tile_done(it);
+                    mbar_arrive(&S.bar_p_full[X]);
                     continue;
                 }
                 if (it == 0) {
@@ -868,10 +607,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 PROF(ps_comp += clock64() - ps_t1;)
-                if (kPingPong && !kQkOnly<MODE>) {
-                    if (X == 0 ? (it < nB) : (it + 1 < nA)) named_bar_arrive(X == 0 ? 4 : 3, 256);
-                }
-                tile_done(it);
+                mbar_arrive(&S.bar_p_full[X]);
             }
             PROF(const long long t_epi0 = clock64();)
 
@@ -1573,19 +1309,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     const int ipg = (P.step + 1) / 2;
     const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
     P.cluster = 1;
-    P.k_rows = static_cast<const uint8_t*>(k);
-    P.v16_rows = static_cast<const uint8_t*>(v16);
-    P.lsu = 0;
-    if (MODE == SPARSE) {
-        if (const char* env = getenv("AA_K3_GATHER")) P.lsu = env[0] == 'l' ? 1 : env[0] == 'a' ? 2 : 0;
-    }
     // K3: cluster the pairs of one (head, group) so each gathered tile is
     // fetched once per cluster (TMA multicast); needs every group complete
     // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
     // Measured with split K / V gather warps (128k Llama): clusters of 2 /
     // 4 -> K3 16.3-16.4 / 17.1-17.3 ms (4-CTA clusters co-schedule on only
     // 132 of 148 SMs); AA_K3_CLUSTER overrides.
-    if (MODE == SPARSE && !P.lsu && P.T_m % P.step == 0) {
+    if (MODE == SPARSE && P.T_m % P.step == 0) {
         int want = 2;
         if (const char* env = getenv("AA_K3_CLUSTER")) want = atoi(env);
         for (int c : {want, 2, 1})
@@ -1613,31 +1343,7 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, fa_pair<MODE>, tq, tk, tv, tkg, tvg, PP);
     };
-    // Clusters of 4 tile only part of the GPU's SMs (GPC sizes are not all
-    // multiples of 4); the lightest groups can go to a concurrent launch with
-    // clusters of 2 that runs on the SMs the first launch cannot use.
-    int split_groups = 0;
-    if (MODE == SPARSE && P.cluster == 4 && ipg % 2 == 0) {
-        if (const char* env = getenv("AA_K3_SPLIT_GROUPS")) split_groups = atoi(env);
-        split_groups = std::max(0, std::min(split_groups, P.groups - 1));
-    }
-    if (split_groups == 0) return launch_cluster(P, grid, s);
-    const unsigned grid2 = static_cast<unsigned>(split_groups * ipg * f.hq);
-    static cudaStream_t side = nullptr;
-    if (!side && (e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking))) return e;
-    cudaEvent_t fork, join;
-    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming))) return e;
-    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming))) return e;
-    FaParams P2 = P;
-    P2.item0 = static_cast<int>(grid - grid2);
-    P2.cluster = 2;
-    if (!(e = cudaEventRecord(fork, s)) && !(e = cudaStreamWaitEvent(side, fork, 0)) &&
-        !(e = launch_cluster(P, grid - grid2, s)) && !(e = launch_cluster(P2, grid2, side)) &&
-        !(e = cudaEventRecord(join, side)))
-        e = cudaStreamWaitEvent(s, join, 0);
-    cudaEventDestroy(fork);
-    cudaEventDestroy(join);
-    return e;
+    return launch_cluster(P, grid, s);
 }
 
 cudaError_t convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s) {

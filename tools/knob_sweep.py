@@ -2,7 +2,7 @@
 """Time the fused chain (bench workload) under runtime knobs read by the
 library through getenv, e.g.
 
-    python tools/knob_sweep.py --env AA_K3_SPLIT_GROUPS=0,8,12,16
+    python tools/knob_sweep.py --env AA_K3_CLUSTER=1,2,4
 
 Prints one JSON line per setting with ms/layer and the per-stage device
 times (CUDA events recorded by the library on its stream)."""
