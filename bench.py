@@ -351,6 +351,31 @@ def run_ours(args):
                 "frac_of_burst_peak": kernels[dom]["tflops"] / tensor_peak_burst,
                 "work": f"4*d*positions = {kernels[dom]['flops']:.4e} FLOP per launch"}
 
+    # the same layer replayed from a CUDA graph (capi.GraphPipeline: every
+    # launch of the chain captured once, no host work per step)
+    graph = None
+    try:
+        del pipe
+        torch.cuda.empty_cache()
+        gp = capi.GraphPipeline(q, k, v, cfg)
+        for _ in range(args.warmup):
+            gp.replay()
+        torch.cuda.synchronize()
+        barrier()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(stream)
+        for _ in range(args.steps):
+            gp.replay()
+        gb.record(stream)
+        torch.cuda.synchronize()
+        graph = {"ms_per_layer": reduce([ga.elapsed_time(gb) / args.steps], "max")[0],
+                 "note": "capi.GraphPipeline: the fused chain captured in a CUDA graph, replayed K times"}
+        del gp
+        torch.cuda.empty_cache()
+        pipe = capi.Pipeline(q, k, v, cfg)
+    except Exception as exc:  # noqa: BLE001 - reported, not fatal
+        graph = {"error": str(exc)}
+
     # recall of the selection at 128k: one dense QK pass (RECALL kernel) over
     # this rank's heads with the stripe lists of the timed configuration
     recall = None
@@ -392,7 +417,7 @@ def run_ours(args):
             hq_h = q.cpu().pin_memory()
             hk = k.cpu().pin_memory()
             hv = v.cpu().pin_memory()
-            del pipe
+            pipe = None
             torch.cuda.empty_cache()
             o_h = torch.empty(hq_h.shape, dtype=torch.float32).pin_memory()
             c_h = torch.empty(hq_h.shape[0], dtype=torch.int64).pin_memory()
@@ -442,6 +467,7 @@ def run_ours(args):
             "kernels": kernels,
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms) if dense_ms else None,
+            "graph": graph,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -190,6 +190,34 @@ class Pipeline:
         return out, computed
 
 
+class GraphPipeline:
+    """The fused chain captured once into a CUDA graph on fixed device
+    buffers (q, k, v, out, computed): ``replay()`` re-runs every launch of
+    aa_anchor_attention (V->f16, K1, pool, K2, compaction, K3, stats) with no
+    host work per step.  Write new inputs into ``q``/``k``/``v`` in place
+    between replays."""
+
+    def __init__(self, q, k, v, cfg: BlockConfig, out_dtype=torch.float32, zero_anchor=False):
+        self.q, self.k, self.v = q, k, v
+        self.pipe = Pipeline(q, k, v, cfg)
+        hq, n, d = q.shape
+        self.out = torch.empty((hq, n, d), dtype=out_dtype, device=q.device)
+        self.computed = torch.empty(hq, dtype=torch.int64, device=q.device)
+        # warm-up outside the capture (one-time attributes, allocator pools)
+        s = torch.cuda.Stream(device=q.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.pipe(q, k, v, zero_anchor=zero_anchor, out=self.out, computed=self.computed)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.pipe(q, k, v, zero_anchor=zero_anchor, out=self.out, computed=self.computed)
+
+    def replay(self):
+        self.graph.replay()
+        return self.out, self.computed
+
+
 STAGES = ("v_to_f16", "k1_anchor", "pool_k2_identify", "k3_sparse", "stats")
 
 

@@ -16,7 +16,10 @@ namespace {
 // the run 32 words (1024 candidates) at a time, staging the step's keys in
 // shared memory in ascending order and writing them out contiguously.  Global traffic: the
 // bits (twice, the second time from L2) plus 4 B per selected key.
-constexpr int kCompactWarps = 8;
+#ifndef AA_COMPACT_WARPS
+#define AA_COMPACT_WARPS 8
+#endif
+constexpr int kCompactWarps = AA_COMPACT_WARPS;
 
 __global__ void __launch_bounds__(kCompactWarps * 32)
     k_compact(Geo geo, int64_t hq, const uint32_t* __restrict__ bits, int64_t words_per_row,

@@ -282,3 +282,25 @@ def test_host_entry_pipelined_equals_device_chain(hq, hkv, pinned):
     assert torch.equal(comp_h, comp.cpu())
     out16, _ = c.anchor_attention_host(q, k, v, cfg, out_dtype=torch.bfloat16)
     assert torch.equal(out16.float(), ref.cpu().bfloat16().float())
+
+
+def test_graph_replay_equals_eager():
+    """The fused chain captured in a CUDA graph (capi.GraphPipeline) replays
+    the eager result exactly, also after the inputs are rewritten in place."""
+    c = capi()
+    n = 8192
+    q, k, v = (x.cuda() for x in gen(n, hq=4, hkv=1, seed=31))
+    cfg = c.BlockConfig()
+    g = c.GraphPipeline(q, k, v, cfg)
+    out, comp = g.replay()
+    torch.cuda.synchronize()
+    ref, ref_comp = c.anchor_attention(q, k, v, cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(comp, ref_comp)
+    q2, k2, v2 = (x.cuda() for x in gen(n, hq=4, hkv=1, seed=32))
+    g.q.copy_(q2), g.k.copy_(k2), g.v.copy_(v2)
+    out, comp = g.replay()
+    torch.cuda.synchronize()
+    ref, ref_comp = c.anchor_attention(q2, k2, v2, cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(comp, ref_comp)
