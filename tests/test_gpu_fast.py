@@ -304,3 +304,33 @@ def test_graph_replay_equals_eager():
     ref, ref_comp = c.anchor_attention(q2, k2, v2, cfg)
     torch.cuda.synchronize()
     assert torch.equal(out, ref) and torch.equal(comp, ref_comp)
+
+
+@pytest.mark.parametrize("hq,step", [(12, 2), (7, 4), (3, 16)])
+def test_identify_mtile_pairs_all_heads(oracle, hq, step):
+    """K2 assigns one CTA per (KV head, pair of 128-row M-tiles of (group,
+    head) rows): 12 heads x 32 groups (step 2) = 3 M-tiles (an odd pair), 7
+    heads x 16 groups = 1 M-tile, 3 heads x 4 groups.  Every head's stripe
+    sets match the oracle outside the +-1e-3 band, and the fused chain's
+    outputs match the oracle for every head."""
+    c = capi()
+    n = 8192
+    q, k, v = gen(n, hq=hq, hkv=1, seed=100 + hq)
+    cfg = c.BlockConfig(128, 128, step, 12.0)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    st = c.compute_anchor(qd, kd, vd, cfg)
+    anchor, qbar = c.pool(qd, kd, st, cfg)
+    idx, counts = c.identify(qd, kd, qbar, anchor, cfg)
+    out, computed = c.anchor_attention(qd, kd, vd, cfg)
+    torch.cuda.synchronize()
+    ocfg = Cfg(128, 128, step, 12.0)
+    kn, vn = k[0].float().numpy(), v[0].float().numpy()
+    idx = idx.cpu().numpy().view(np.uint32)
+    counts = counts.cpu().numpy()
+    for h in range(hq):
+        qn = q[h].float().numpy()
+        same = band_equal(oracle, qn, kn, ocfg, None, idx[h], counts[h])
+        r = oracle.anchor_attention(qn, kn, vn, ocfg)
+        assert_out_close(out[h].cpu().numpy(), r["out"], f"head {h}")
+        if same:
+            assert int(computed[h]) == r["computed"], h
