@@ -112,6 +112,28 @@ def measured_peaks():
         return {}
 
 
+def model_name(hq, hkv):
+    return {(32, 8): "Llama-3.1-8B", (28, 4): "Qwen2.5-7B"}.get((hq, hkv), "GQA")
+
+
+def config_ref(args):
+    """Which BASELINE.json config this run is."""
+    if (args.hq, args.hkv) == (28, 4):
+        return "BASELINE configs[4]"
+    if (args.hq, args.hkv) == (32, 8):
+        if args.n == 32768:
+            return "BASELINE configs[1]"
+        if args.n == 131072:
+            return "BASELINE configs[3]" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else \
+                "BASELINE configs[2]"
+    return "off-baseline shape"
+
+
+def workload_str(args):
+    return (f"{model_name(args.hq, args.hkv)} attention {args.hq}Q/{args.hkv}KV d=128, n={args.n}, "
+            f"theta={args.theta}, b=128, step={args.step_blocks} ({config_ref(args)})")
+
+
 def layer_geometry(n, step):
     """covered positions and stripe candidates per head (closed form)."""
     from paper_2505_23520_b200 import capi
@@ -192,8 +214,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"Llama-3.1-8B attention 32Q/8KV d=128, n={args.n}, theta={args.theta}, "
-                               f"b=128, step={args.step_blocks}", "global_batch": 1,
+        "config": {"workload": workload_str(args), "global_batch": 1,
                    "seq_len": args.n, "parallelism": "host threads over heads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
@@ -235,19 +256,25 @@ def run_ours(args):
                             group=host_group)
         return t.tolist()
 
-    if args.hkv % world:
-        raise SystemExit(f"hkv={args.hkv} must be divisible by the rank count {world}")
-    rep = args.hq // args.hkv
-    kv_local = args.hkv // world
-    kv0 = rank * kv_local
+    from paper_2505_23520_b200.sharding import shard_heads
 
-    # this rank's KV heads and their query heads; each KV head is generated from
-    # its own seed so the data does not depend on the rank count
+    try:
+        shard = shard_heads(args.hq, args.hkv, rank, world)
+    except ValueError as exc:
+        raise SystemExit(f"cannot shard {args.hq}/{args.hkv} heads over {world} ranks: {exc}")
+    rep = args.hq // args.hkv
+    kv_local = shard.kv_heads
+
+    # this rank's KV heads and their query heads (KV-head blocks, or with more
+    # ranks than KV heads a run of one KV head's query heads); each KV head is
+    # generated from its own seed so the data does not depend on the rank count
     qs, ks, vs = [], [], []
-    for kvh in range(kv0, kv0 + kv_local):
+    for kvh in range(shard.kv_begin, shard.kv_end):
         q, k, v = gen_sink_workload(SinkWorkloadSpec(n=args.n, hq=rep, hkv=1,
                                                      seed=args.seed + kvh), device=dev)
-        qs.append(q), ks.append(k), vs.append(v)
+        lo = max(shard.q_begin - kvh * rep, 0)
+        hi = min(shard.q_end - kvh * rep, rep)
+        qs.append(q[lo:hi].contiguous()), ks.append(k), vs.append(v)
     q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
     del qs, ks, vs
     cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
@@ -455,11 +482,11 @@ def run_ours(args):
             "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"Llama-3.1-8B attention 32Q/8KV d=128, n={args.n}, "
-                                   f"theta={args.theta}, b=128, step={args.step_blocks} "
-                                   "(BASELINE configs[2])",
+            "config": {"workload": workload_str(args),
                        "global_batch": 1, "seq_len": args.n,
-                       "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"kv-head shard x{world}" if world <= args.hkv else
+                                       f"query-head runs of each KV head x{world}") if world > 1
+                                      else "single GPU",
                        "l2": f"inputs larger than L2 (q/k/v {(args.hq + 2 * args.hkv) * args.n * D * 2 / 1e9:.2f} "
                              "GB per layer vs 126 MB L2), no flush"},
             "sparsity": sparsity, "recall": recall, "computed_positions": comp_total,

@@ -13,7 +13,8 @@ from paper_2505_23520_b200.sharding import (gather_heads, local_slices, max_over
 
 
 def test_shard_assignment_covers_heads_once():
-    for hq, hkv, world in [(32, 8, 1), (32, 8, 2), (32, 8, 4), (32, 8, 8), (28, 4, 2), (28, 4, 4)]:
+    for hq, hkv, world in [(32, 8, 1), (32, 8, 2), (32, 8, 4), (32, 8, 8), (28, 4, 2), (28, 4, 4),
+                           (28, 4, 8), (32, 8, 16), (8, 2, 8)]:
         seen_q, seen_kv = [], []
         for r in range(world):
             s = shard_heads(hq, hkv, r, world)
@@ -21,9 +22,17 @@ def test_shard_assignment_covers_heads_once():
             seen_kv += list(range(s.kv_begin, s.kv_end))
             for h in range(s.q_begin, s.q_end):  # GQA: query head reads a local KV head
                 assert s.kv_begin <= h // (hq // hkv) < s.kv_end
-        assert seen_q == list(range(hq)) and seen_kv == list(range(hkv))
+        assert seen_q == list(range(hq))
+        if world <= hkv:
+            assert seen_kv == list(range(hkv))
+        else:  # query-head runs: each KV head replicated on world / hkv ranks
+            assert seen_kv == sorted(seen_kv) and sorted(set(seen_kv)) == list(range(hkv))
+    # query-head runs: Qwen2.5-7B (28 Q / 4 KV) over 8 ranks -> 4 / 3 heads each
+    assert [shard_heads(28, 4, r, 8).q_heads for r in range(8)] == [3, 4] * 4
     with pytest.raises(ValueError):
-        shard_heads(28, 4, 0, 8)
+        shard_heads(28, 4, 0, 6)   # 6 ranks: neither divides nor is a multiple of 4 KV heads
+    with pytest.raises(ValueError):
+        shard_heads(8, 2, 0, 16)   # more ranks than query heads
 
 
 def _free_port():
@@ -42,7 +51,8 @@ def _worker(rank, world, port, q, k, v, ret):
     ql, kl, vl = local_slices(q, k, v, shard)
     rep = q.shape[0] // k.shape[0]
     # stand-in per-head op with the same head->KV-head dependence as attention
-    out_local = ql * kl.repeat_interleave(rep, 0) + vl.repeat_interleave(rep, 0)
+    kv_of = torch.tensor([h // rep - shard.kv_begin for h in range(shard.q_begin, shard.q_end)])
+    out_local = ql * kl[kv_of] + vl[kv_of]
     full = gather_heads(out_local)
     t = max_over_ranks(float(rank + 1))
     if rank == 0:
@@ -51,17 +61,20 @@ def _worker(rank, world, port, q, k, v, ret):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_gather_and_max():
-    world = 2
-    q = torch.randn(8, 16, 4)
-    k = torch.randn(2, 16, 4)
-    v = torch.randn(2, 16, 4)
+@pytest.mark.parametrize("world,hq,hkv", [(2, 8, 2), (4, 6, 2)])
+def test_gloo_gather_and_max(world, hq, hkv):
+    """world 2: KV-head blocks; world 4 over 2 KV heads: query-head runs of
+    unequal length (3 query heads per KV head -> 1 / 2), gathered padded."""
+    q = torch.randn(hq, 16, 4)
+    k = torch.randn(hkv, 16, 4)
+    v = torch.randn(hkv, 16, 4)
     mgr = mp.Manager()
     ret = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), q, k, v, ret), nprocs=world, join=True)
-    expect = q * k.repeat_interleave(4, 0) + v.repeat_interleave(4, 0)
+    rep = hq // hkv
+    expect = q * k.repeat_interleave(rep, 0) + v.repeat_interleave(rep, 0)
     assert torch.equal(ret["full"], expect)
-    assert ret["max"] == 2.0
+    assert ret["max"] == float(world)
 
 
 @pytest.mark.gpu
@@ -72,7 +85,7 @@ def test_sharded_layer_equals_full_layer():
     q, k, v = gen_sink_workload(SinkWorkloadSpec(n=8192, hq=8, hkv=4, seed=17), device="cuda")
     cfg = capi.BlockConfig()
     full, comp = capi.anchor_attention(q, k, v, cfg)
-    for world in (2, 4):
+    for world in (2, 4, 8):  # 8 ranks over 4 KV heads: query-head runs
         parts, comps = [], []
         for r in range(world):
             s = shard_heads(8, 4, r, world)
