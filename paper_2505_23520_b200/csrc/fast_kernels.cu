@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // the whole warp runs the loop; one elected lane issues (warp-uniform operands)
             constexpr uint64_t kDescHi = sdesc_sw128_hi(1024);
             const uint32_t la0 = sdesc_sw128_lo(smem_u32(S.a[0][0]), 16);
             const uint32_t lk0 = sdesc_sw128_lo(smem_u32(S.k[0]), 16);
@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                     const int b = nk % kIdStages;
                     PROF(const long long t0 = clock64();)
                     mbar_wait(&S.bar_k_full[b], (nk / kIdStages) & 1);
-                    PROF(atomicAdd(&g_prof[5][1], clock64() - t0); atomicAdd(&g_prof[5][9], 1ull);)
+                    PROF(if (lane == 0) { atomicAdd(&g_prof[5][1], clock64() - t0); atomicAdd(&g_prof[5][9], 1ull); })
                     const uint32_t lk = lk0 + b * (kTileBytes >> 4);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
@@ -1014,25 +1014,25 @@ __global__ void __launch_bounds__(kIdThreads, 1)
                         const int sb = ns[m] & 1;
                         PROF(const long long t0 = clock64();)
                         if (ns[m] >= 2) mbar_wait(&S.bar_s_empty[m][sb], ((ns[m] >> 1) - 1) & 1);
-                        PROF(atomicAdd(&g_prof[5][2], clock64() - t0);)
+                        PROF(if (lane == 0) atomicAdd(&g_prof[5][2], clock64() - t0);)
                         tc_fence_after();
                         const uint32_t lhi = la0 + m * (2 * kTileBytes >> 4), llo = lhi + (kTileBytes >> 4);
                         const uint32_t d_tmem = tmem + (2 * m + sb) * 128;
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
                             const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
-                            mma_ss(d_tmem, kDescHi | (lhi + off), kDescHi | (lk + off), kIdescQK,
+                            mma_ss_w(d_tmem, kDescHi | (lhi + off), kDescHi | (lk + off), kIdescQK,
                                    kk > 0 ? 1u : 0u);
                         }
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
                             const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
-                            mma_ss(d_tmem, kDescHi | (llo + off), kDescHi | (lk + off), kIdescQK, 1u);
+                            mma_ss_w(d_tmem, kDescHi | (llo + off), kDescHi | (lk + off), kIdescQK, 1u);
                         }
-                        mma_commit(&S.bar_s_full[m][sb]);
+                        mma_commit_w(&S.bar_s_full[m][sb]);
                         ++ns[m];
                     }
-                    mma_commit(&S.bar_k_empty[b]);
+                    mma_commit_w(&S.bar_k_empty[b]);
                 }
             }
         }
