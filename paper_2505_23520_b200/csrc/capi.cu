@@ -57,6 +57,8 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // Selection-bitmask row pitch in 32-bit words (multiple of 4: 16-byte stores).
 int64_t words_per_row(int64_t n) { return ((n + 31) / 32 + 3) / 4 * 4; }
 
+aa::FastArgs fast_args(const aa_problem& p);
+
 // Buffers of the fused chain, carved from one workspace.
 struct Carve {
     size_t off = 0;
@@ -70,7 +72,8 @@ struct Carve {
 
 struct Layout {
     void *m, *l, *acc, *qsum, *msum, *anchor, *qbar, *offsets, *bits, *indices, *counts, *taken,
-        *v16;
+        *v16, *split;
+    size_t split_bytes;
     int64_t words_per_row;
     size_t total;
 };
@@ -97,6 +100,9 @@ Layout carve(const aa_problem& p, const aa_plan& plan, void* ws) {
     L.counts = c.take(hq * G * 4);
     L.taken = c.take(hq * 8);
     L.v16 = p.dtype == AA_BF16 ? c.take(static_cast<size_t>(p.hkv) * n * d * 2) : nullptr;
+    // K2's split A operand (q_bar = hi + lo, bf16) of the fast path
+    L.split_bytes = p.dtype == AA_BF16 ? aa::fast_identify_scratch_bytes(fast_args(p)) : 0;
+    L.split = L.split_bytes ? c.take(L.split_bytes) : nullptr;
     L.total = c.off;
     return L;
 }
@@ -149,6 +155,19 @@ aa_status require_device() {
         return fail(AA_ERR_CUDA, std::string("no CUDA device available (") +
                                      cudaGetErrorString(e) +
                                      "); anchorattn has no CPU fallback");
+    // Stage-API temporaries come from the stream-ordered pool; keep its memory
+    // mapped across synchronisations (the default threshold 0 unmaps it at
+    // every sync and the next cudaMallocAsync remaps, a host stall).
+    static thread_local int pooled_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != pooled_dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pooled_dev = dev;
+    }
     return AA_OK;
 }
 
@@ -321,14 +340,16 @@ aa_status aa_pool(const aa_problem* p, const void* q, const void* m, const float
 static aa_status identify_impl(const aa_problem* p, const aa_plan& plan, const void* k,
                                const float* qbar, const double* anchor, int zero_anchor,
                                uint32_t* indices, int32_t* counts, int64_t* offsets_dev,
-                               uint32_t* bits, int64_t words_per_row, cudaStream_t st) {
+                               uint32_t* bits, int64_t words_per_row, cudaStream_t st,
+                               void* scratch = nullptr, size_t scratch_bytes = 0) {
     const aa::Geo G = geo_of(p->n, p->cfg);
     const double* ref = zero_anchor ? nullptr : anchor;
     if (p->dtype == AA_F32) {
         AA_CUDA(aa::launch_identify_exact(exact_args(*p), static_cast<const float*>(k), qbar, ref,
                                           bits, words_per_row, st));
     } else {
-        AA_CUDA(aa::fast_identify(fast_args(*p), k, qbar, ref, bits, words_per_row, st));
+        AA_CUDA(aa::fast_identify(fast_args(*p), k, qbar, ref, bits, words_per_row, st, scratch,
+                                  scratch_bytes));
     }
     AA_CUDA(aa::launch_offsets(G, offsets_dev, st));
     AA_CUDA(aa::launch_compact(G, p->hq, bits, words_per_row, offsets_dev,
@@ -494,7 +515,8 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
                                     static_cast<uint32_t*>(L.indices),
                                     static_cast<int32_t*>(L.counts),
                                     static_cast<int64_t*>(L.offsets),
-                                    static_cast<uint32_t*>(L.bits), L.words_per_row, st))
+                                    static_cast<uint32_t*>(L.bits), L.words_per_row, st, L.split,
+                                    L.split_bytes))
         return s;
     mark(3, st);
     AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),

@@ -36,7 +36,10 @@ cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const fl
 // K2 — Alg. 2 scoring + threshold, one selection bit per candidate.
 cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
                           const double* anchor, uint32_t* bits, int64_t words_per_row,
-                          cudaStream_t s);
+                          cudaStream_t s,
+                          void* scratch = nullptr, size_t scratch_bytes = 0);
+// Bytes of K2's split A operand (pass as scratch to skip the stream-ordered allocation).
+size_t fast_identify_scratch_bytes(const FastArgs& f);
 // K3 — Alg. 3 gathered-stripe fold resumed from (m, l, acc).
 cudaError_t fast_sparse(const FastArgs& f, const void* q, const void* k, const void* v16,
                         const float* m, const float* l, const float* acc,

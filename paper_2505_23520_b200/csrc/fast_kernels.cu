@@ -1381,9 +1381,15 @@ cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const fl
     return cudaGetLastError();
 }
 
+size_t fast_identify_scratch_bytes(const FastArgs& f) {
+    const int64_t rows = f.geo.groups() * f.rep;
+    const int64_t rows_pad = (rows + kB - 1) / kB * kB;
+    return static_cast<size_t>(2 * f.hkv) * rows_pad * kD * 2;
+}
+
 cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
                           const double* anchor, uint32_t* bits, int64_t words_per_row,
-                          cudaStream_t s) {
+                          cudaStream_t s, void* scratch, size_t scratch_bytes) {
     const int64_t G = f.geo.groups();
     const int64_t max_end = f.geo.middle_end(G - 1);
     const int64_t span = max_end > f.geo.b_kv ? max_end - f.geo.b_kv : 0;
@@ -1392,10 +1398,11 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     if (words_per_row % 4) return cudaErrorInvalidValue;  // 16-byte word stores
     const int rows = static_cast<int>(G * f.rep);
     const int rows_pad = (rows + kB - 1) / kB * kB;
-    void* split = nullptr;
+    void* split = scratch;
     cudaError_t e;
     const size_t split_bytes = static_cast<size_t>(2 * f.hkv) * rows_pad * kD * 2;
-    if ((e = cudaMallocAsync(&split, split_bytes, s))) return e;
+    const bool own = scratch == nullptr || scratch_bytes < split_bytes;
+    if (own && (e = cudaMallocAsync(&split, split_bytes, s))) return e;
     k_split_qbar<<<dim3(static_cast<unsigned>(rows_pad), static_cast<unsigned>(f.hkv)), kD, 0, s>>>(
         static_cast<int>(G), static_cast<int>(f.rep), rows_pad, qbar,
         static_cast<__nv_bfloat16*>(split));
@@ -1404,7 +1411,7 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
                          static_cast<int64_t>(rows_pad) * kD)) ||
         (e = make_map_3d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f.geo.n, f.hkv, f.kv_rs,
                          f.kv_hs))) {
-        cudaFreeAsync(split, s);
+        if (own) cudaFreeAsync(split, s);
         return e;
     }
     constexpr size_t smem = sizeof(IdSmem) + 1024;
@@ -1414,7 +1421,7 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     if (!attr) {
         if ((e = cudaFuncSetAttribute(k_identify_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)))) {
-            cudaFreeAsync(split, s);
+            if (own) cudaFreeAsync(split, s);
             return e;
         }
         int dev = 0;
@@ -1435,7 +1442,7 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     k_identify_tc<<<grid, kIdThreads, smem, s>>>(ta, tk, w, anchor, f.theta, bits, words_per_row);
     stage_mark(7, s);
     e = cudaGetLastError();
-    cudaFreeAsync(split, s);
+    if (own) cudaFreeAsync(split, s);
     return e;
 }
 
