@@ -677,37 +677,71 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 // column sums are done), 128 rows x 64 f32 per half, 16-B chunks
                 // XOR-swizzled by row
                 if (P.qsum != nullptr && nX > 0) mbar_wait(&S.bar_qsum, 0);
-                float* stg = reinterpret_cast<float*>(S.q[X]);
-                const int rows_valid = min(kB, P.n - qx * kB);
-                const size_t gbase = (static_cast<size_t>(h) * P.n + qx * kB) * kD;
-                for (int half = 0; half < 2; ++half) {
-                    if (half) named_bar_sync(1 + X, 128);  // half 0 drained from the staging buffer
-                    uint32_t v[64];
-                    tmem_ld32(tO + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-                    tmem_ld32(tO + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-                    tmem_wait_ld();
+                if (P.acc_f16) {
+                    // acc / l in f16, staged in this tile's Q buffer (its last
+                    // QK has completed, the column sums are done) in the
+                    // 128B-swizzled layout of a TMA box {64, 128}, then two
+                    // TMA stores (async; rows past n are clipped by the map)
+                    uint8_t* stg = S.q[X];
 #pragma unroll
-                    for (int ch = 0; ch < 16; ++ch)
-                        *reinterpret_cast<float4*>(stg + r * 64 + ((ch ^ (r & 15)) << 2)) = make_float4(
-                            __uint_as_float(v[4 * ch]) * sv, __uint_as_float(v[4 * ch + 1]) * sv,
-                            __uint_as_float(v[4 * ch + 2]) * sv, __uint_as_float(v[4 * ch + 3]) * sv);
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld32(tO + ch * 32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c8 = 0; c8 < 4; ++c8) {  // 8 columns = one 16-B chunk
+                            const int col = ch * 32 + c8 * 8;
+                            uint4 w;
+                            w.x = pack_half2(__uint_as_float(v[c8 * 8 + 0]) * sv, __uint_as_float(v[c8 * 8 + 1]) * sv);
+                            w.y = pack_half2(__uint_as_float(v[c8 * 8 + 2]) * sv, __uint_as_float(v[c8 * 8 + 3]) * sv);
+                            w.z = pack_half2(__uint_as_float(v[c8 * 8 + 4]) * sv, __uint_as_float(v[c8 * 8 + 5]) * sv);
+                            w.w = pack_half2(__uint_as_float(v[c8 * 8 + 6]) * sv, __uint_as_float(v[c8 * 8 + 7]) * sv);
+                            const int chunk = (col & 63) >> 3;
+                            *reinterpret_cast<uint4*>(stg + (col >> 6) * kAtomBytes + r * 128 +
+                                                      ((chunk ^ (r & 7)) << 4)) = w;
+                        }
+                    }
+                    fence_proxy_async_smem();
                     named_bar_sync(1 + X, 128);
-                    // thread r copies float4 i*128 + r (row idx/16, chunk idx%16): a
-                    // warp instruction spans two rows' 256 contiguous bytes
-                    const int ch = r & 15;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int rr = (i * kB + r) >> 4;
-                        const float4 o = *reinterpret_cast<const float4*>(stg + rr * 64 + ((ch ^ (rr & 15)) << 2));
-                        if (rr < rows_valid) {
-                            const size_t ge = gbase + static_cast<size_t>(rr) * kD + half * 64 + ch * 4;
-                            if (P.acc_f16) {
-                                uint2 w;
-                                w.x = pack_half2(o.x, o.y);
-                                w.y = pack_half2(o.z, o.w);
-                                *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(P.acc_out) + ge) = w;
-                            } else {
-                                *reinterpret_cast<float4*>(P.acc_out + ge) = o;
+                    if (quad == 0 && lane == 0) {
+                        tma_store_3d(&tmVg, stg, 0, qx * kB, h);
+                        tma_store_3d(&tmVg, stg + kAtomBytes, 64, qx * kB, h);
+                        tma_store_commit();
+                        tma_store_wait_read();  // the CTA may exit once the box is read
+                    }
+                } else {  // f32 acc (the stage API's AnchorState::acc): coalesced LSU stores
+                    float* stg = reinterpret_cast<float*>(S.q[X]);
+                    const int rows_valid = min(kB, P.n - qx * kB);
+                    const size_t gbase = (static_cast<size_t>(h) * P.n + qx * kB) * kD;
+                    for (int half = 0; half < 2; ++half) {
+                        if (half) named_bar_sync(1 + X, 128);  // half 0 drained from the staging buffer
+                        uint32_t v[64];
+                        tmem_ld32(tO + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                        tmem_ld32(tO + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                        tmem_wait_ld();
+    #pragma unroll
+                        for (int ch = 0; ch < 16; ++ch)
+                            *reinterpret_cast<float4*>(stg + r * 64 + ((ch ^ (r & 15)) << 2)) = make_float4(
+                                __uint_as_float(v[4 * ch]) * sv, __uint_as_float(v[4 * ch + 1]) * sv,
+                                __uint_as_float(v[4 * ch + 2]) * sv, __uint_as_float(v[4 * ch + 3]) * sv);
+                        named_bar_sync(1 + X, 128);
+                        // thread r copies float4 i*128 + r (row idx/16, chunk idx%16): a
+                        // warp instruction spans two rows' 256 contiguous bytes
+                        const int ch = r & 15;
+    #pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int rr = (i * kB + r) >> 4;
+                            const float4 o = *reinterpret_cast<const float4*>(stg + rr * 64 + ((ch ^ (rr & 15)) << 2));
+                            if (rr < rows_valid) {
+                                const size_t ge = gbase + static_cast<size_t>(rr) * kD + half * 64 + ch * 4;
+                                if (P.acc_f16) {
+                                    uint2 w;
+                                    w.x = pack_half2(o.x, o.y);
+                                    w.y = pack_half2(o.z, o.w);
+                                    *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(P.acc_out) + ge) = w;
+                                } else {
+                                    *reinterpret_cast<float4*>(P.acc_out + ge) = o;
+                                }
                             }
                         }
                     }
@@ -1287,7 +1321,14 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     if ((e = make_map_3d(&tv, v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, n, f.hkv, kD, n * kD))) return e;
     const int64_t krows = ((f.hkv - 1) * f.kv_hs + (n - 1) * f.kv_rs) / kD + 1;
     if ((e = make_map_gather(&tkg, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, krows))) return e;
-    if ((e = make_map_gather(&tvg, v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, f.hkv * n))) return e;
+    if (MODE == ANCHOR && P.acc_f16) {
+        // K1's f16 acc / l leaves by TMA store: the 5th map (the V gather map
+        // of K3, unused here) describes acc_out [hq, n, d] f16
+        if ((e = make_map_3d(&tvg, P.acc_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, n, f.hq, kD, n * kD)))
+            return e;
+    } else if ((e = make_map_gather(&tvg, v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, f.hkv * n))) {
+        return e;
+    }
     P.n = static_cast<int>(n);
     P.hq = static_cast<int>(f.hq);
     P.rep = static_cast<int>(f.rep);
