@@ -129,7 +129,7 @@ struct PairSmem {
     uint8_t q[2][kTileBytes];
     uint8_t k[kKStages][kTileBytes];
     uint8_t v[2][kTileBytes];
-    uint64_t bar_q, bar_qsum;
+    uint64_t bar_q, bar_qsum, bar_acc[2];
     uint64_t bar_k_full[kKStages], bar_k_empty[kKStages], bar_v_full[2], bar_v_empty[2];
     uint64_t bar_s_full[2], bar_p_full[2], bar_o_done[2];  // per query tile
     uint32_t tmem_base;
@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(&S.bar_q, 1);
         mbar_init(&S.bar_qsum, 64);
+        mbar_init(&S.bar_acc[0], 1);
+        mbar_init(&S.bar_acc[1], 1);
         for (int b = 0; b < kKStages; ++b) {
             mbar_init(&S.bar_k_full[b], 1);
             mbar_init(&S.bar_k_empty[b], C);
@@ -625,8 +627,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             // in flight at once, instead of chunk by chunk behind each TMEM read
             float pre_m = 0.f, pre_l = 1.f;
             const bool prefetch = MODE == SPARSE && P.acc_f16;
-            // ... and the acc / l tile in the coalesced order of the staged
-            // pass below (thread r: 8 B at float4 slot i*128 + r of each half)
+            // ... and (bf16 output) the acc / l tile in the coalesced order of
+            // the staged pass below (thread r: 8 B at float4 slot i*128 + r)
             uint2 pre_a[2][16];
             if (prefetch) {
                 if (row < P.n) {
@@ -634,7 +636,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     pre_m = P.m_in[ri];
                     pre_l = P.l_in[ri];
                 }
-                const int rows_v = min(kB, P.n - qx * kB);
+                const int rows_v = P.out_bf16 ? min(kB, P.n - qx * kB) : 0;  // f32 out: TMA path
                 const __half* acc_h = reinterpret_cast<const __half*>(P.acc_in) +
                                       (static_cast<size_t>(h) * P.n + qx * kB) * kD;
 #pragma unroll
@@ -751,6 +753,67 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     P.msum[static_cast<size_t>(h) * P.T_m + qx] =
                         static_cast<double>(S.red[X][0][0]) + S.red[X][0][1] + S.red[X][0][2] + S.red[X][0][3];
                 }
+            } else if (MODE == SPARSE && P.acc_f16 && !P.out_bf16) {
+                // merge with K1's state (f16 acc / l) entirely through TMA:
+                //   out = O * (fs * inv) + acc_n * (la * fa * inv)
+                // acc_n tile -> a free K stage (every QK is complete), then per
+                // row (thread = TMEM lane = row) the merged f32 values go to a
+                // staging buffer in the 128B-swizzled box layout {32, 128} and
+                // leave by TMA store, 64 columns at a time (Q_X for columns
+                // 0-63, a V stage PV no longer reads for columns 64-127)
+                const float ma2 = pre_m * kLog2e;
+                const float M = fmaxf(ma2, m_used);
+                const float fa = ex2(ma2 - M);
+                const float fs = (m_used == -INFINITY) ? 0.f : ex2(m_used - M);
+                const float inv = 1.f / (pre_l * fa + l * fs);
+                const float so = fs * inv, sa = pre_l * fa * inv;
+                const bool issue = quad == 0 && lane == 0;
+                uint8_t* accb = S.k[X];
+                if (issue) {
+                    mbar_expect_tx(&S.bar_acc[X], kTileBytes);
+                    tma_load_3d(accb, &tmK, &S.bar_acc[X], 0, qx * kB, h);
+                    tma_load_3d(accb + kAtomBytes, &tmK, &S.bar_acc[X], 64, qx * kB, h);
+                }
+                mbar_wait(&S.bar_acc[X], 0);
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint8_t* dst = half ? S.v[X ? ((nX - 1) & 1) : (nX & 1)] : S.q[X];
+                    uint32_t v[64];
+                    if (nX > 0) {
+                        tmem_ld32(tO + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                        tmem_ld32(tO + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 64; ++jj) v[jj] = 0u;
+                    }
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; ++c8) {  // 8 columns: one 16-B f16 chunk of acc
+                        const uint4 araw = *reinterpret_cast<const uint4*>(
+                            accb + half * kAtomBytes + r * 128 + ((c8 ^ (r & 7)) << 4));
+                        const __half2* a2 = reinterpret_cast<const __half2*>(&araw);
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {  // two f32 16-B chunks
+                            const float2 a01 = __half22float2(a2[2 * u]);
+                            const float2 a23 = __half22float2(a2[2 * u + 1]);
+                            const int c = c8 * 8 + u * 4;  // column within the half (0..63)
+                            const float4 o = make_float4(
+                                __uint_as_float(v[c]) * so + a01.x * sa, __uint_as_float(v[c + 1]) * so + a01.y * sa,
+                                __uint_as_float(v[c + 2]) * so + a23.x * sa, __uint_as_float(v[c + 3]) * so + a23.y * sa);
+                            const int chunk = (c & 31) >> 2;
+                            *reinterpret_cast<float4*>(dst + (c >> 5) * kAtomBytes + r * 128 +
+                                                       ((chunk ^ (r & 7)) << 4)) = o;
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1 + X, 128);
+                    if (issue) {
+                        tma_store_3d(&tmV, dst, half * 64, qx * kB, h);
+                        tma_store_3d(&tmV, dst + kAtomBytes, half * 64 + 32, qx * kB, h);
+                        tma_store_commit();
+                    }
+                }
+                if (issue) tma_store_wait_read();  // the CTA may exit once both halves are read
             } else if (MODE == SPARSE && P.acc_f16) {
                 // merge with K1's state (f16 acc / l hand-off) and leave through
                 // shared memory so that loads and stores are coalesced:
@@ -1292,6 +1355,21 @@ cudaError_t make_map_3d(CUtensorMap* m, const void* base, CUtensorMapDataType dt
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 3-D map {d, rows, heads} of f32, box {32, 128, 1} (128 B rows), 128B swizzle.
+cudaError_t make_map_3d_f32(CUtensorMap* m, const void* base, int64_t rows, int64_t heads) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kD), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(heads)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kD * 4), static_cast<cuuint64_t>(rows * kD * 4)};
+    const cuuint32_t box[3] = {32, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // 2-D map {d, total_rows} (row pitch d elements) for gather4, box {64, 1}.
 cudaError_t make_map_gather(CUtensorMap* m, const void* base, CUtensorMapDataType dt,
                             int64_t total_rows) {
@@ -1321,6 +1399,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     if ((e = make_map_3d(&tv, v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, n, f.hkv, kD, n * kD))) return e;
     const int64_t krows = ((f.hkv - 1) * f.kv_hs + (n - 1) * f.kv_rs) / kD + 1;
     if ((e = make_map_gather(&tkg, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, krows))) return e;
+    if (MODE == SPARSE && P.acc_f16 && !P.out_bf16) {
+        // K3's merge epilogue moves by TMA: the tile maps of K and V (unused
+        // by the gathering K3) describe K1's f16 acc / l [hq, n, d] (load) and
+        // the f32 output [hq, n, d] (store)
+        if ((e = make_map_3d(&tk, P.acc_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, n, f.hq, kD, n * kD))) return e;
+        if ((e = make_map_3d_f32(&tv, P.out, n, f.hq))) return e;
+    }
     if (MODE == ANCHOR && P.acc_f16) {
         // K1's f16 acc / l leaves by TMA store: the 5th map (the V gather map
         // of K3, unused here) describes acc_out [hq, n, d] f16
