@@ -229,6 +229,29 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             mbar_init(&S.bar_o_done[b], 1);
         }
         fence_mbar_init();
+        // The loads that need no peer: the Q pair and (contiguous-tile modes)
+        // the first K / V tile go out now, overlapping the TMEM allocation
+        // and the (cluster) barrier below.
+        if (ntiles > 0) {
+            mbar_expect_tx(&S.bar_q, hasB ? 2 * kTileBytes : kTileBytes);
+            tma_load_3d(S.q[0], &tmQ, &S.bar_q, 0, qA * kB, h);
+            tma_load_3d(S.q[0] + kAtomBytes, &tmQ, &S.bar_q, 64, qA * kB, h);
+            if (hasB) {
+                tma_load_3d(S.q[1], &tmQ, &S.bar_q, 0, qB * kB, h);
+                tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
+            }
+            if (MODE != SPARSE) {
+                const int kt = kv_tile_of(MODE, 0, wsb);
+                mbar_expect_tx(&S.bar_k_full[0], kTileBytes);
+                tma_load_3d(S.k[0], &tmK, &S.bar_k_full[0], 0, kt * kB, kvh);
+                tma_load_3d(S.k[0] + kAtomBytes, &tmK, &S.bar_k_full[0], 64, kt * kB, kvh);
+                if (!kQkOnly<MODE>) {
+                    mbar_expect_tx(&S.bar_v_full[0], kTileBytes);
+                    tma_load_3d(S.v[0], &tmV, &S.bar_v_full[0], 0, kt * kB, kvh);
+                    tma_load_3d(S.v[0] + kAtomBytes, &tmV, &S.bar_v_full[0], 64, kt * kB, kvh);
+                }
+            }
+        }
     }
     if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
@@ -283,19 +306,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     if (warp == 0) {
         setmaxnreg_dec<56>();
         // ------------------------------------------------------------ producer
-        if (lane == 0 && ntiles > 0) {
-            mbar_expect_tx(&S.bar_q, hasB ? 2 * kTileBytes : kTileBytes);
-            tma_load_3d(S.q[0], &tmQ, &S.bar_q, 0, qA * kB, h);
-            tma_load_3d(S.q[0] + kAtomBytes, &tmQ, &S.bar_q, 64, qA * kB, h);
-            if (hasB) {
-                tma_load_3d(S.q[1], &tmQ, &S.bar_q, 0, qB * kB, h);
-                tma_load_3d(S.q[1] + kAtomBytes, &tmQ, &S.bar_q, 64, qB * kB, h);
-            }
-        }
+        // (the Q pair and the first contiguous K / V tile were issued at init)
         if (MODE == SPARSE) {
             gather_split(true);  // V rows: warp 3
         } else if (MODE != SPARSE) {
-            for (int it = 0; it < ntiles; ++it) {
+            for (int it = 1; it < ntiles; ++it) {
                 if (lane == 0) {
                     const int st = it & 1;
                     const int sk = it % kKStages;
