@@ -334,3 +334,20 @@ def test_identify_mtile_pairs_all_heads(oracle, hq, step):
         assert_out_close(out[h].cpu().numpy(), r["out"], f"head {h}")
         if same:
             assert int(computed[h]) == r["computed"], h
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 127, 128, 129, 255])
+def test_tiny_sequences(oracle, n):
+    """Sequences shorter than / around one 128-row block: partial tiles, no
+    middle region, a single group — the fused chain and the stage API agree
+    with the oracle."""
+    c = capi()
+    q, k, v = gen(n, hq=2, hkv=1, seed=n)
+    cfg = c.BlockConfig(128, 128, 16, 12.0)
+    out, computed = c.anchor_attention(q.cuda(), k.cuda(), v.cuda(), cfg)
+    torch.cuda.synchronize()
+    for h in range(2):
+        r = oracle.anchor_attention(q[h].float().numpy(), k[0].float().numpy(), v[0].float().numpy(),
+                                    Cfg(128, 128, 16, 12.0))
+        assert_out_close(out[h].cpu().numpy(), r["out"], f"n={n} head {h}")
+        assert int(computed[h]) == r["computed"]
