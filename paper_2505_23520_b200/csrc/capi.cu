@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/anchorattn_capi.h"
 #include "common.cuh"
@@ -582,16 +583,45 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
         }
     }
     const int64_t rep = p->hkv > 0 ? p->hq / p->hkv : 1;
-    const int64_t per = p->hkv > 0 ? (p->hkv + kMaxChunks - 1) / kMaxChunks : 1;  // KV heads per chunk
-    const int nchunks = p->hkv > 0 ? static_cast<int>((p->hkv + per - 1) / per) : 0;
+    // Chunks: blocks of whole KV heads, or — with fewer KV heads than chunks
+    // (e.g. one KV head per rank under sharding) — runs of one KV head's
+    // query heads, the first run of each KV head carrying its K / V copy.
+    struct Chunk {
+        int64_t kv0, nkv, h0, nh;
+        bool copy_kv;
+    };
+    std::vector<Chunk> chunks;
+    int64_t max_nkv = 0, max_nh = 0;
+    if (p->hkv >= kMaxChunks || rep == 1) {
+        const int64_t per = p->hkv > 0 ? (p->hkv + kMaxChunks - 1) / kMaxChunks : 1;  // KV heads per chunk
+        for (int64_t kv0 = 0; kv0 < p->hkv; kv0 += per) {
+            const int64_t nkv = std::min(per, p->hkv - kv0);
+            chunks.push_back({kv0, nkv, kv0 * rep, nkv * rep, true});
+        }
+    } else {
+        const int64_t parts = std::min<int64_t>(rep, std::max<int64_t>(1, kMaxChunks / p->hkv));
+        for (int64_t kvh = 0; kvh < p->hkv; ++kvh)
+            for (int64_t part = 0; part < parts; ++part) {
+                const int64_t a0 = part * rep / parts, a1 = (part + 1) * rep / parts;
+                if (a1 > a0) chunks.push_back({kvh, 1, kvh * rep + a0, a1 - a0, part == 0});
+            }
+    }
+    for (const Chunk& ch : chunks) {
+        max_nkv = std::max(max_nkv, ch.nkv);
+        max_nh = std::max(max_nh, ch.nh);
+    }
+    const int nchunks = static_cast<int>(chunks.size());
+    if (nchunks > kMaxChunks) return fail(AA_ERR_INVALID_ARGUMENT, "aa_anchor_attention_host: chunking");
     aa_problem sub = *p;
     sub.q_row_stride = sub.kv_row_stride = p->d;
     sub.q_head_stride = sub.kv_head_stride = p->n * p->d;
-    sub.hkv = per;
-    sub.hq = per * rep;
     aa_plan sub_plan;
-    if (nchunks > 0)
+    if (nchunks > 0) {
+        // workspace for the largest chunk (a run's query heads share one KV head)
+        sub.hkv = max_nkv;
+        sub.hq = max_nkv == 1 ? max_nh : max_nkv * rep;
         if (aa_status s = aa_make_plan(&sub, &sub_plan)) return s;
+    }
     const size_t es = p->dtype == AA_BF16 ? 2 : 4;
     const size_t os = out_dtype == AA_BF16 ? 2 : 4;
     const size_t head_in = static_cast<size_t>(p->n * p->d) * es;
@@ -621,14 +651,14 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     const char* hv_ = static_cast<const char*>(v);
     char* ho_ = static_cast<char*>(out);
     for (int c = 0; c < nchunks; ++c) {
-        const int64_t kv0 = c * per;
-        const int64_t nkv = std::min(per, p->hkv - kv0);
-        const int64_t h0 = kv0 * rep, nh = nkv * rep;
+        const int64_t kv0 = chunks[c].kv0, nkv = chunks[c].nkv, h0 = chunks[c].h0, nh = chunks[c].nh;
         const size_t qo = static_cast<size_t>(h0) * head_in, qn = static_cast<size_t>(nh) * head_in;
         const size_t ko = static_cast<size_t>(kv0) * head_in, kn = static_cast<size_t>(nkv) * head_in;
         AA_CUDA(cudaMemcpyAsync(dq + qo, hq_ + qo, qn, cudaMemcpyHostToDevice, st_in));
-        AA_CUDA(cudaMemcpyAsync(dk + ko, hk_ + ko, kn, cudaMemcpyHostToDevice, st_in));
-        AA_CUDA(cudaMemcpyAsync(dv + ko, hv_ + ko, kn, cudaMemcpyHostToDevice, st_in));
+        if (chunks[c].copy_kv) {
+            AA_CUDA(cudaMemcpyAsync(dk + ko, hk_ + ko, kn, cudaMemcpyHostToDevice, st_in));
+            AA_CUDA(cudaMemcpyAsync(dv + ko, hv_ + ko, kn, cudaMemcpyHostToDevice, st_in));
+        }
         AA_CUDA(cudaEventRecord(ev_in[c], st_in));
         AA_CUDA(cudaStreamWaitEvent(st_c, ev_in[c], 0));
         sub.hkv = nkv;
