@@ -69,7 +69,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 // 8 prologue (to the first S), 9 CTAs, 10 producer wait-empty, 11/12
 // softmax-B wait-S / compute.
 #ifdef AA_PROF
-__device__ unsigned long long g_prof[6][16];  // [fa_pair MODE | 5 = K2 identify][slot]
+__device__ unsigned long long g_prof[6][32];  // [fa_pair MODE | 5 = K2 identify][slot]
 #define PROF(...) __VA_ARGS__
 #else
 #define PROF(...)
@@ -253,6 +253,21 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
         }
     }
+    // K3 gather warps (0: K rows, 3: V rows) read the first stripe tile's row
+    // indices before the (cluster) barrier; later tiles' one tile ahead
+    const int g_lanes = 32 / C;
+    const int g_row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
+    auto stripe_rows = [&](int it, bool isK, int (&r)[4]) {
+        const int base = it * kB;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = base + g_row0 + u;
+            const int j = lane < g_lanes ? static_cast<int>(list[e < count ? e : base]) : 0;
+            r[u] = isK ? kvh * P.kv_head_rows + j * P.kv_row_rows : kvh * P.n + j;
+        }
+    };
+    int pre_r[4] = {0, 0, 0, 0};
+    if (MODE == SPARSE && ntiles > 0 && (warp == 0 || warp == 3)) stripe_rows(0, warp == 0, pre_r);
     if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
     if (C > 1) cluster_sync(); else __syncthreads();
@@ -266,22 +281,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // halves); in a cluster of C each CTA gathers rows [crank*128/C, +128/C)
     // of a tile and multicasts them to the C CTAs.
     auto gather_split = [&](bool isK) {
-        const int lanes = 32 / C;
-        const bool gl = lane < lanes;
-        const int row0 = static_cast<int>(crank) * (kB / C) + lane * 4;
-        const int vh = kvh * P.n;  // V16 scratch is packed [hkv, n, d]
+        const bool gl = lane < g_lanes;
+        int r[4] = {pre_r[0], pre_r[1], pre_r[2], pre_r[3]};
         for (int it = 0; it < ntiles; ++it) {
             const int st = isK ? it % kKStages : it & 1;
             const int ph = isK ? it / kKStages : it >> 1;
             const int depth = isK ? kKStages : 2;
-            int r[4];
-            const int base = it * kB;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = base + row0 + u;
-                const int j = gl ? static_cast<int>(list[e < count ? e : base]) : 0;
-                r[u] = isK ? kvh * P.kv_head_rows + j * P.kv_row_rows : vh + j;
-            }
             uint64_t* full = isK ? &S.bar_k_full[st] : &S.bar_v_full[st];
             uint64_t* empty = isK ? &S.bar_k_empty[st] : &S.bar_v_empty[st];
             if (lane == 0) {
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 mbar_expect_tx(full, kTileBytes);
             }
             __syncwarp();
-            uint8_t* dst = (isK ? S.k[st] : S.v[st]) + row0 * 128;
+            uint8_t* dst = (isK ? S.k[st] : S.v[st]) + g_row0 * 128;
             const CUtensorMap* tm = isK ? &tmKg : &tmVg;
             if (gl) {
                 if (C > 1) {
@@ -300,6 +305,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     tma_gather4(dst + kAtomBytes, tm, full, 64, r[0], r[1], r[2], r[3]);
                 }
             }
+            if (it + 1 < ntiles) stripe_rows(it + 1, isK, r);  // next tile's rows, ahead of its stage
         }
     };
 
@@ -515,6 +521,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
                 tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
                 tmem_wait_ld();
+                PROF(if (lane == 0 && warp == 4) {
+                    reg_fence32(&v[96]);
+                    atomicAdd(&g_prof[MODE][16], clock64() - ps_t1);
+                })
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) mask_chunk(ch);
                 if constexpr (MODE == TILEMASS) {
@@ -1689,9 +1699,9 @@ cudaError_t fast_tile_mass(const FastArgs& f, const void* q, const void* k, floa
 #ifdef AA_PROF
 extern "C" int aa_prof_read(unsigned long long* out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, aa::g_prof, sizeof(unsigned long long) * 96) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, aa::g_prof, sizeof(unsigned long long) * 192) != cudaSuccess) return -1;
     if (reset) {
-        static const unsigned long long z[96] = {};
+        static const unsigned long long z[192] = {};
         if (cudaMemcpyToSymbol(aa::g_prof, z, sizeof(z)) != cudaSuccess) return -1;
     }
     return 0;

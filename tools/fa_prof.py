@@ -56,7 +56,7 @@ def main():
 
     L = capi.lib()
     L.aa_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-    buf = (C.c_ulonglong * 96)()
+    buf = (C.c_ulonglong * 192)()
 
     def report(name, v):
         ctas = max(1, v[9])
@@ -68,6 +68,7 @@ def main():
             row[s + "_per_cta"] = round(v[i] / ctas)
         row["smA_compute_per_tile"] = round(v[1] / tiles)
         row["epi_wait_odone_per_cta"] = round(v[13] / ctas)
+        row["smA_tmem_ld_per_tile"] = round(v[16] / tiles)
         row["epi_t_staged0"] = round(v[14] / ctas)
         row["epi_t_half0_done"] = round(v[15] / ctas)
 
@@ -94,7 +95,7 @@ def main():
         assert L.aa_prof_read(buf, 1) == 0
         allv = list(buf)
         for name, mode in (("k1_anchor", 0), ("k3_sparse " + os.environ.get("AA_K3_GATHER", "tma"), 1)):
-            report(name, allv[16 * mode:16 * mode + 16])
+            report(name, allv[32 * mode:32 * mode + 32])
         if not a.no_dense and rnd == 0:
             nd = min(a.n, 32768)
             L.aa_prof_read(buf, 1)
@@ -102,7 +103,7 @@ def main():
                                  v[:, :nd].contiguous(), out_dtype=torch.bfloat16)
             torch.cuda.synchronize()
             assert L.aa_prof_read(buf, 1) == 0
-            report(f"dense n={nd}", list(buf)[32:48])
+            report(f"dense n={nd}", list(buf)[64:96])
 
 
 if __name__ == "__main__":

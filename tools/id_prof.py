@@ -17,7 +17,7 @@ from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload 
 
 L = capi.lib()
 L.aa_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * 96)()
+buf = (C.c_ulonglong * 192)()
 n, hq, hkv = 131072, 32, 8
 dev = torch.device("cuda", 0)
 qs, ks, vs = [], [], []
@@ -32,7 +32,7 @@ for _ in range(3):
     L.aa_prof_read(buf, 1)
     capi.identify(q, k, qbar, anchor, cfg)
     assert L.aa_prof_read(buf, 1) == 0
-    x = list(buf)[80:96]
+    x = list(buf)[160:192]
     ctas, tiles, epi_tiles = max(1, x[7]), max(1, x[9]), max(1, x[5])
     print(json.dumps({"ctas": x[7], "k_tiles": x[9], "cta_cycles": x[6] // ctas,
                       "prod_wait_empty_per_tile": x[0] / tiles, "mma_wait_k_per_tile": x[1] / tiles,
