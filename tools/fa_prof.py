@@ -94,7 +94,7 @@ def main():
         torch.cuda.synchronize()
         assert L.aa_prof_read(buf, 1) == 0
         allv = list(buf)
-        for name, mode in (("k1_anchor", 0), ("k3_sparse " + os.environ.get("AA_K3_GATHER", "tma"), 1)):
+        for name, mode in (("k1_anchor", 0), ("k3_sparse", 1)):
             report(name, allv[32 * mode:32 * mode + 32])
         if not a.no_dense and rnd == 0:
             nd = min(a.n, 32768)
