@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             auto pv = [&](int X, int j) {
                 const int st = j & 1;
                 PROF(const long long t0 = clock64();)
-                mbar_wait(&S.bar_p_full[X], j & 1);
+                mbar_wait_handoff(&S.bar_p_full[X], j & 1);
                 PROF(const long long t1 = clock64(); pw_p += t1 - t0;)
                 if (kQkOnly<MODE>) return;  // S_X(j) consumed; no PV
                 mbar_wait(&S.bar_v_full[st], (j >> 1) & 1);
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     if (kt == qx) lim = min(lim, r + 1);
                 }
                 PROF(const long long ps_t0 = clock64();)
-                mbar_wait(&S.bar_s_full[X], it & 1);
+                mbar_wait_handoff(&S.bar_s_full[X], it & 1);
                 PROF(ps_t1 = clock64(); ps_wait += ps_t1 - ps_t0; if (it == 0) ps_first = ps_t1;)
                 tc_fence_after();
                 // single pass: the whole S row in registers

@@ -47,6 +47,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Hand-off waits on the critical softmax <-> MMA path.  AA_HANDOFF_WAIT:
+// 0 = try_wait (hardware-suspended), 1 = test_wait spin, 2 = try_wait with a
+// short suspend-time hint.
+#ifndef AA_HANDOFF_WAIT
+#define AA_HANDOFF_WAIT 0
+#endif
+__device__ __forceinline__ void mbar_wait_handoff(uint64_t* bar, uint32_t parity) {
+#if AA_HANDOFF_WAIT == 1
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#elif AA_HANDOFF_WAIT == 2
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 32;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
