@@ -351,3 +351,25 @@ def test_tiny_sequences(oracle, n):
                                     Cfg(128, 128, 16, 12.0))
         assert_out_close(out[h].cpu().numpy(), r["out"], f"n={n} head {h}")
         assert int(computed[h]) == r["computed"]
+
+
+def test_fast_path_deterministic_and_recall_at_32k():
+    """R/tests/test_sparse_exec.cpp:192-212 on the tcgen05 path at 32k (4 query
+    heads / 1 KV head): two runs are bitwise identical, and on the sink /
+    stripe heads the selection keeps recall >= 0.99 (GPU recall pass over
+    covered ∪ stripes) at sparsity > 0.5."""
+    c = capi()
+    n = 32768
+    q, k, v = (x.cuda() for x in gen(n, hq=4, hkv=1, seed=77))
+    cfg = c.BlockConfig()
+    o1, c1 = c.anchor_attention(q, k, v, cfg)
+    o2, c2 = c.anchor_attention(q, k, v, cfg)
+    st = c.compute_anchor(q, k, v, cfg)
+    anchor, qbar = c.pool(q, k, st, cfg)
+    idx, counts = c.identify(q, k, qbar, anchor, cfg)
+    rec = c.union_recall(q, k, idx, counts, cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(c1, c2)
+    sparsity = 1.0 - c1.double() / (n * (n + 1) / 2)
+    assert float(rec.min()) >= 0.99, rec
+    assert float(sparsity.min()) > 0.5, sparsity
