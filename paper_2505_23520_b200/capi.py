@@ -271,16 +271,23 @@ def pool(q, k, state, cfg=BlockConfig(), use_partials=True):
     return anchor, qbar
 
 
-def identify(q, k, qbar, anchor, cfg=BlockConfig(), zero_anchor=False):
-    """Alg. 2: returns (indices [hq, capacity] u32-as-int32, counts [hq, G] int32)."""
+def identify(q, k, qbar, anchor, cfg=BlockConfig(), zero_anchor=False, out=None, workspace=None):
+    """Alg. 2: returns (indices [hq, capacity] u32-as-int32, counts [hq, G] int32).
+    ``out=(indices, counts)`` and a ``workspace`` (uint8, >= plan.workspace_bytes)
+    may be passed to keep allocations out of timed loops."""
     p = make_problem(q, k, cfg)
     pl = plan(p)
     hq = q.shape[0]
     cap = max(pl.stripe_capacity, 1)
-    idx = torch.zeros((hq, cap), dtype=torch.int32, device=q.device)
-    counts = torch.zeros((hq, pl.groups), dtype=torch.int32, device=q.device)
+    if out is None:
+        idx = torch.zeros((hq, cap), dtype=torch.int32, device=q.device)
+        counts = torch.zeros((hq, pl.groups), dtype=torch.int32, device=q.device)
+    else:
+        idx, counts = out
+    ws = workspace if workspace is not None else None
     _check(lib().aa_identify(C.byref(p), _ptr(k), _ptr(qbar), _ptr(anchor), int(zero_anchor),
-                             _ptr(idx), _ptr(counts), None, 0, _stream()))
+                             _ptr(idx), _ptr(counts), _ptr(ws), ws.numel() if ws is not None else 0,
+                             _stream()))
     return idx, counts
 
 
