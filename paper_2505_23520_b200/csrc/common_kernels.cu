@@ -14,8 +14,9 @@ namespace {
 // warps, each owning a contiguous run of bit-words: pass 1 counts the run's
 // selected keys, a block scan gives each run its output offset, pass 2 walks
 // the run 32 words (1024 candidates) at a time, staging the step's keys in
-// shared memory in ascending order and writing them out contiguously.  Global traffic: the
-// bits (twice, the second time from L2) plus 4 B per selected key.
+// shared memory in ascending order and writing them out contiguously.
+// Global traffic: the bits (twice, the second time from L2) plus 4 B per
+// selected key.
 #ifndef AA_COMPACT_WARPS
 #define AA_COMPACT_WARPS 8
 #endif
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kCompactWarps * 32)
         // highest set bit first, written from the end of this lane's slots
         int pos = incl;
         const uint32_t key0 = static_cast<uint32_t>(geo.b_kv + ((w0 + lane) << 5));
-        while (word) {
+        while (word) {  // (a fixed 32-step predicated loop measured 53 vs 43 us)
             const int b = 31 - __clz(word);
             stg[--pos] = key0 + static_cast<uint32_t>(b);
             word ^= 1u << b;
