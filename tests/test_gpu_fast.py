@@ -120,17 +120,20 @@ def test_golden_fixtures_bf16():
         assert int(computed[0]) == int(z["computed"]), name
 
 
-def test_gqa_multihead_and_sharded_heads(oracle):
-    """8 query heads over 2 KV heads; spot-check two heads of different KV groups."""
+@pytest.mark.parametrize("hq,hkv,heads", [(8, 2, (1, 6)), (28, 4, (0, 13, 27))])
+def test_gqa_multihead_and_sharded_heads(oracle, hq, hkv, heads):
+    """GQA through the fused chain (Llama-like 4:1 and Qwen2.5-like 7:1
+    ratios); spot-check heads of different KV groups against the oracle."""
     c = capi()
     n = 4096
-    q, k, v = gen(n, hq=8, hkv=2, seed=21)
+    rep = hq // hkv
+    q, k, v = gen(n, hq=hq, hkv=hkv, seed=21 + hq)
     cfg = c.BlockConfig()
     out, computed = c.anchor_attention(q.cuda(), k.cuda(), v.cuda(), cfg)
     torch.cuda.synchronize()
-    for h in (1, 6):
-        r = oracle.anchor_attention(q[h].float().numpy(), k[h // 4].float().numpy(),
-                                    v[h // 4].float().numpy(), Cfg())
+    for h in heads:
+        r = oracle.anchor_attention(q[h].float().numpy(), k[h // rep].float().numpy(),
+                                    v[h // rep].float().numpy(), Cfg())
         assert_out_close(out[h].cpu().numpy(), r["out"], f"head {h}")
 
 
