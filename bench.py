@@ -460,8 +460,28 @@ def run_ours(args):
             h2d, d2h = (int(x) for x in reduce(
                 [(hq_h.numel() + hk.numel() + hv.numel()) * 2, o_h.numel() * 4 + c_h.numel() * 8],
                 "sum"))
+            # the copy floor: the same bytes moved alone (H2D of q/k/v and
+            # D2H of O on two streams at once, no kernels), best of 3
+            dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            do = torch.empty(o_h.shape, dtype=torch.float32, device=dev)
+            s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            floor = []
+            for _ in range(3):
+                torch.cuda.synchronize()
+                tt = time.perf_counter()
+                with torch.cuda.stream(s_in):
+                    for d_, h_ in ((dq, hq_h), (dk, hk), (dv, hv)):
+                        d_.copy_(h_, non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    o_h.copy_(do, non_blocking=True)
+                torch.cuda.synchronize()
+                floor.append((time.perf_counter() - tt) * 1e3)
+            del dq, dk, dv, do
+            floor_ms = reduce([min(floor)], "max")[0]
             e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h,
+                   "copy_floor_ms": floor_ms,
+                   "copy_floor": "same H2D+D2H bytes alone on two streams, no kernels",
                    "path": "aa_anchor_attention_host (pinned host q/k/v -> device chain -> host out f32)"}
         except Exception as exc:  # noqa: BLE001 - reported in the line
             e2e = {"value": None, "unit": UNIT, "error": str(exc)}

@@ -163,7 +163,7 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
  * convention, bindings.cpp:21-32): copies q/k/v in, runs, copies out and the
  * per-head computed counts back; blocks until done.  Device buffers are
  * cached across calls of the same size.  The copies are pipelined against the
- * chain over up to 16 chunks — blocks of KV heads, or runs of one KV head's
+ * chain over up to 32 chunks — blocks of KV heads, or runs of one KV head's
  * query heads when there are fewer KV heads than chunks — on copy-in, compute
  * and copy-out streams, so with page-locked host buffers the PCIe traffic
  * overlaps the kernels. */

@@ -561,7 +561,7 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     static void* dbuf = nullptr;
     static size_t dbytes = 0;
     static cudaStream_t st_in = nullptr, st_c = nullptr, st_out = nullptr;
-    constexpr int kMaxChunks = 16;
+    constexpr int kMaxChunks = 32;
     static cudaEvent_t ev_in[kMaxChunks], ev_done[kMaxChunks];
     std::lock_guard<std::mutex> lock(mu);
     aa_plan plan;
