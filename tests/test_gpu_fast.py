@@ -266,7 +266,8 @@ def test_dense_tile_mass_matches_softmax(n):
         assert abs(mass[h].sum() - n) <= 1e-2 * n / 1000
 
 
-@pytest.mark.parametrize("hq,hkv,pinned", [(8, 2, True), (36, 12, True), (4, 4, False), (7, 1, True)])
+@pytest.mark.parametrize("hq,hkv,pinned", [(8, 2, True), (36, 12, True), (4, 4, False), (7, 1, True),
+                                           (66, 33, True)])
 def test_host_entry_pipelined_equals_device_chain(hq, hkv, pinned):
     """aa_anchor_attention_host (KV-head chunks pipelined over three streams)
     returns exactly the device chain's output and per-head computed counts —
