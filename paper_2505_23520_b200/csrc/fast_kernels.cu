@@ -67,7 +67,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 // through aa_prof_read).  Slots: 0/1 softmax-A wait-S / compute, 2 softmax-A
 // tiles, 3/4/5 MMA wait P / K / V, 6 CTA cycles, 7 epilogue (softmax A),
 // 8 prologue (to the first S), 9 CTAs, 10 producer wait-empty, 11/12
-// softmax-B wait-S / compute.
+// softmax-B wait-S / compute; 20/21/22 ~first CTA start / last CTA end /
+// sum of CTA lifetimes (globaltimer ns).
 #ifdef AA_PROF
 __device__ unsigned long long g_prof[6][32];  // [fa_pair MODE | 5 = K2 identify][slot]
 #define PROF(...) __VA_ARGS__
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                                                ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    PROF(const long long t_cta0 = clock64();)
+    PROF(const long long t_cta0 = clock64(); unsigned long long ns_cta0;
+         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_cta0));)
 
     // work item: heavy-first (last groups first).  Within a group, the pairs of
     // one head are adjacent, then the heads of one KV head: CTAs that run
@@ -992,6 +994,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     PROF(if (threadIdx.x == 0) {
         atomicAdd(&g_prof[MODE][6], clock64() - t_cta0);
         atomicAdd(&g_prof[MODE][9], 1ull);
+        // SM occupancy: sum of CTA lifetimes vs the launch span (globaltimer)
+        unsigned long long ns1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
+        atomicMax(&g_prof[MODE][20], ~ns_cta0);
+        atomicMax(&g_prof[MODE][21], ns1);
+        atomicAdd(&g_prof[MODE][22], ns1 - ns_cta0);
     })
 }
 

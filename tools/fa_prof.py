@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--build-only", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--sms", type=int, default=148, help="CTA slots (1 CTA / SM)")
     ap.add_argument("--lib", default=PROF_LIB, help="a -DAA_PROF build of the library")
     a = ap.parse_args()
     if a.build_only:
@@ -73,6 +74,11 @@ def main():
         row["epi_t_half0_done"] = round(v[15] / ctas)
 
         row["smA_wait_per_tile"] = round(v[0] / tiles)
+        if v[21]:
+            span = v[21] - ((1 << 64) - 1 - v[20])
+            row["span_us"] = round(span / 1e3, 1)
+            row["cta_us"] = round(v[22] / ctas / 1e3, 2)
+            row["sm_busy"] = round(v[22] / (a.sms * span), 4)  # CTA-resident share (1 CTA / SM)
         row["lib"] = os.path.basename(a.lib)
         print(json.dumps(row), flush=True)
 
