@@ -150,6 +150,33 @@ def layer_geometry(n, step):
     return covered, cand
 
 
+def layer_tiles(q, k, v, args, cfg):
+    """128x128 tiles K1 and K3 execute on this rank's heads: K1 runs block 0
+    plus the window [wsb(g), qb] for every query block (fa_pair<ANCHOR>'s
+    loop bounds); K3 runs ceil(f_c(g) / 128) gathered tiles for each query
+    block of group g (counts from one stage-API identify, outside the timed
+    region)."""
+    import torch
+
+    from paper_2505_23520_b200 import capi
+
+    n, step, hq = args.n, args.step_blocks, q.shape[0]
+    T = (n + 127) // 128
+    k1 = 0
+    for qb in range(T):
+        rb = (qb // step) * step * 128
+        wsb = 1 if rb < 256 else rb // 128 - 1
+        k1 += 1 + (qb - wsb + 1 if qb >= wsb else 0)
+    st = capi.compute_anchor(q, k, v, cfg)
+    anchor, qbar = capi.pool(q, k, st, cfg)
+    del st
+    _, cnt = capi.identify(q, k, qbar, anchor, cfg)
+    G = cnt.shape[1]
+    qtiles = [min(step, T - g * step) for g in range(G)]
+    k3 = int(((cnt.long() + 127) // 128).cpu().sum(0).mul(torch.tensor(qtiles, dtype=torch.int64)).sum())
+    return hq * k1, k3
+
+
 def reference_sample(n_sample, heads, theta, step, seed, threads=None):
     """Run the reference (oracle/_ref) anchor_attention on `heads` heads of the
     synthetic workload at n_sample through its own parallel_for.  Returns
@@ -337,11 +364,18 @@ def run_ours(args):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     k1_flops = 4.0 * D * hq_local * covered
     k3_flops = 4.0 * D * (comp_local - hq_local * covered)
+    # tile-executed work beside the algorithmic figures: every
+    # 128x128 tile a kernel runs costs 4*128^3 FLOP (QK + PV) whatever the
+    # causal / tail masks leave of it
+    tile_fl = 4.0 * 128 ** 3
+    k1_tiles, k3_tiles = layer_tiles(q, k, v, args, cfg)
     kernels = {
         "k1_anchor": {"ms": stage_ms[1], "flops": k1_flops,
-                      "tflops": k1_flops / (stage_ms[1] * 1e-3) / 1e12},
+                      "tflops": k1_flops / (stage_ms[1] * 1e-3) / 1e12,
+                      "tiles": k1_tiles, "tile_tflops": k1_tiles * tile_fl / (stage_ms[1] * 1e-3) / 1e12},
         "k3_sparse": {"ms": stage_ms[3], "flops": k3_flops,
-                      "tflops": k3_flops / (stage_ms[3] * 1e-3) / 1e12},
+                      "tflops": k3_flops / (stage_ms[3] * 1e-3) / 1e12,
+                      "tiles": k3_tiles, "tile_tflops": k3_tiles * tile_fl / (stage_ms[3] * 1e-3) / 1e12},
     }
     # K2 algorithmic bytes: K over the widest middle region once
     # per KV head + pooled q (f32) and anchor (f64) per (head, group)
