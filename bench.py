@@ -177,6 +177,28 @@ def layer_tiles(q, k, v, args, cfg):
     return hq * k1, k3
 
 
+def k2_mma_flops(args, kv_heads):
+    """Executed MMA work of k_identify_tc: per KV head and 128-row M-tile of
+    (group, head) rows, key tiles up to the widest middle region of its groups,
+    two bf16 MMAs (q_bar hi and lo) of 2*128^3 FLOP per key tile."""
+    import ctypes as C
+
+    from paper_2505_23520_b200 import capi
+
+    cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
+    c = cfg.c()
+    L = capi.lib()
+    G = L.aa_group_count(args.n, C.byref(c))
+    rep = args.hq // args.hkv
+    n_mt = (G * rep + 127) // 128
+    tiles = 0
+    for mt in range(n_mt):
+        g_last = min(G - 1, ((mt + 1) * 128 - 1) // rep)
+        span = L.aa_middle_end_token(g_last, C.byref(c), args.n) - 128
+        tiles += max(0, (span + 127) // 128)
+    return kv_heads * tiles * 2 * 2.0 * 128 ** 3
+
+
 def reference_sample(n_sample, heads, theta, step, seed, threads=None):
     """Run the reference (oracle/_ref) anchor_attention on `heads` heads of the
     synthetic workload at n_sample through its own parallel_for.  Returns
@@ -389,7 +411,11 @@ def run_ours(args):
                               "gbs": k2_bytes / (k2_kernel_ms * 1e-3) / 1e9,
                               "frac_hbm": k2_bytes / (k2_kernel_ms * 1e-3) / 1e9 / hbm_peak,
                               "hbm_peak_gbs": hbm_peak,
-                              "note": "k_identify_tc alone (events 6->7); bound: HBM"}
+                              "frac_spec_8tbs": k2_bytes / (k2_kernel_ms * 1e-3) / 1e9 / 8000.0,
+                              "mma_tflops": k2_mma_flops(args, kv_local) / (k2_kernel_ms * 1e-3) / 1e12,
+                              "note": "k_identify_tc alone (events 6->7); HBM bytes are the "
+                                      "algorithmic figure; mma_tflops counts the executed hi + lo "
+                                      "bf16 MMAs of the split q_bar (the other pipe it keeps busy)"}
     kernels["k2_stage"] = {"ms": stage_ms[2], "bytes": k2_bytes,
                            "gbs": k2_bytes / (stage_ms[2] * 1e-3) / 1e9,
                            "note": "pool + q_bar split + identify + offsets + compaction"}
