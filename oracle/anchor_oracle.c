@@ -100,14 +100,49 @@ int64_t ao_anchor_region(int64_t qb, const ao_cfg* c, int64_t n, int64_t* blocks
     return cnt;
 }
 
+/* Dot products of one f32 query row against KT_W keys held transposed as
+ * f64 kt[t * KT_W + u]: the loop over t is outermost, so the KT_W running
+ * sums vectorise across keys while each key's sum still adds its d products
+ * in index order t = 0 .. d-1 — the reference's order (anchor_pass.cpp:66-72,
+ * stripe_identify.cpp:35-40, sparse_exec.cpp:85-92).  The product of two f32
+ * values is exact in f64, so every sum equals the sequential scalar loop bit
+ * for bit; only the evaluation order across DIFFERENT keys changes. */
+#define KT_W 32
+
+static void kt_load(const float* k, int64_t d, const int64_t* rows, int64_t cnt, double* kt) {
+    for (int64_t t = 0; t < d; ++t)
+        for (int64_t u = 0; u < KT_W; ++u)
+            kt[t * KT_W + u] = u < cnt ? (double)k[rows[u] * d + t] : 0.0;
+}
+
+static void kt_load_range(const float* k, int64_t d, int64_t j0, int64_t cnt, double* kt) {
+    for (int64_t t = 0; t < d; ++t)
+        for (int64_t u = 0; u < KT_W; ++u)
+            kt[t * KT_W + u] = u < cnt ? (double)k[(j0 + u) * d + t] : 0.0;
+}
+
+static void kt_dots(const float* q_row, int64_t d, const double* kt, double* out) {
+    double s[KT_W];
+    for (int u = 0; u < KT_W; ++u) s[u] = 0.0;
+    for (int64_t t = 0; t < d; ++t) {
+        const double qt = (double)q_row[t];
+        const double* kr = kt + t * KT_W;
+        for (int u = 0; u < KT_W; ++u) s[u] += qt * kr[u];
+    }
+    for (int u = 0; u < KT_W; ++u) out[u] = s[u];
+}
+
 /* R/src/anchor_pass.cpp:37-96 — per query block, per region block, per row:
  * dot (:66-74), block max, alpha = exp(m - m_new) (0 while m = -inf, :77-78),
- * rescale acc, accumulate p * v (:82-90), l = l * alpha + l_block (:91). */
+ * rescale acc, accumulate p * v (:82-90), l = l * alpha + l_block (:91).
+ * The region block's keys are transposed once (kt_load_range) and shared by
+ * the block's rows. */
 void ao_compute_anchor(int64_t n, int64_t d, const float* q, const float* k, const float* v,
                        const ao_cfg* c, double* m, double* l, double* acc) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
     const int64_t t_m = ceil_div(n, c->b_q);
     const int64_t t_n = ceil_div(n, c->b_kv);
+    const int64_t nsub = ceil_div(c->b_kv, KT_W);
     for (int64_t i = 0; i < n; ++i) {
         m[i] = -INFINITY;
         l[i] = 0.0;
@@ -115,7 +150,8 @@ void ao_compute_anchor(int64_t n, int64_t d, const float* q, const float* k, con
     memset(acc, 0, (size_t)(n * d) * sizeof(double));
 #pragma omp parallel
     {
-        double* qk = (double*)malloc((size_t)c->b_kv * sizeof(double));
+        double* qk = (double*)malloc((size_t)(nsub * KT_W) * sizeof(double));
+        double* kt = (double*)malloc((size_t)(nsub * KT_W * d) * sizeof(double));
         int64_t* blocks = (int64_t*)malloc((size_t)(t_n + 2) * sizeof(int64_t));
 #pragma omp for schedule(dynamic, 1)
         for (int64_t qb = 0; qb < t_m; ++qb) {
@@ -125,27 +161,30 @@ void ao_compute_anchor(int64_t n, int64_t d, const float* q, const float* k, con
             for (int64_t bi = 0; bi < nb; ++bi) {
                 const int64_t key_begin = blocks[bi] * c->b_kv;
                 const int64_t key_end = min64(key_begin + c->b_kv, n);
+                for (int64_t sb = 0; sb < nsub; ++sb) {
+                    const int64_t j0 = key_begin + sb * KT_W;
+                    if (j0 < key_end) kt_load_range(k, d, j0, min64(KT_W, key_end - j0), kt + sb * KT_W * d);
+                }
                 for (int64_t i = row_begin; i < row_end; ++i) {
                     const int64_t causal_end = min64(key_end, i + 1);
                     if (key_begin >= causal_end) continue;
-                    const float* q_row = q + i * d;
+                    const int64_t cols = causal_end - key_begin;
+                    for (int64_t sb = 0; sb * KT_W < cols; ++sb)
+                        kt_dots(q + i * d, d, kt + sb * KT_W * d, qk + sb * KT_W);
                     double block_max = -INFINITY;
-                    for (int64_t j = key_begin; j < causal_end; ++j) {
-                        double sum = 0.0;
-                        const float* k_row = k + j * d;
-                        for (int64_t t = 0; t < d; ++t) sum += (double)q_row[t] * (double)k_row[t];
-                        qk[j - key_begin] = sum * inv_sqrt_d;
-                        if (qk[j - key_begin] > block_max) block_max = qk[j - key_begin];
+                    for (int64_t jj = 0; jj < cols; ++jj) {
+                        qk[jj] = qk[jj] * inv_sqrt_d;
+                        if (qk[jj] > block_max) block_max = qk[jj];
                     }
                     const double m_new = m[i] > block_max ? m[i] : block_max;
                     const double alpha = isinf(m[i]) ? 0.0 : exp(m[i] - m_new);
                     double l_block = 0.0;
                     double* acc_row = acc + i * d;
                     for (int64_t t = 0; t < d; ++t) acc_row[t] *= alpha;
-                    for (int64_t j = key_begin; j < causal_end; ++j) {
-                        const double p = exp(qk[j - key_begin] - m_new);
+                    for (int64_t jj = 0; jj < cols; ++jj) {
+                        const double p = exp(qk[jj] - m_new);
                         l_block += p;
-                        const float* v_row = v + j * d;
+                        const float* v_row = v + (key_begin + jj) * d;
                         for (int64_t t = 0; t < d; ++t) acc_row[t] += p * (double)v_row[t];
                     }
                     l[i] = l[i] * alpha + l_block;
@@ -154,6 +193,7 @@ void ao_compute_anchor(int64_t n, int64_t d, const float* q, const float* k, con
             }
         }
         free(qk);
+        free(kt);
         free(blocks);
     }
 }
@@ -219,71 +259,115 @@ void ao_identify(int64_t n, int64_t d, const float* q, const float* k, const dou
 
 /* R/src/sparse_exec.cpp:13-124 with FoldPlan{chunk, shuffle_seed = 0}:
  * resume (m, l, acc), per row fold each chunk of the group's list, skipping
- * j > i (:79) and anchor-covered j (:82), then O = acc / l (:114-120). */
+ * j > i (:79) and anchor-covered j (:82), then O = acc / l (:114-120).
+ *
+ * The kept entries of a chunk do not depend on the row: a listed j is folded
+ * iff b_kv <= j < window_start(g), and a non-empty [b_kv, window_start(g))
+ * implies window_start(g) <= row_begin(g) - b_kv (geometry.hpp:55-64), so
+ * j < i for every row of the group.  Each chunk is therefore filtered once
+ * and its keys transposed once per block of ROWS rows. */
+#define ROWS 16
+
 int64_t ao_sparse_attention(int64_t n, int64_t d, const float* q, const float* k, const float* v,
                             const ao_cfg* c, const double* m_in, const double* l_in,
                             const double* acc_in, const uint32_t* idx, const int64_t* counts,
                             int64_t chunk, float* out) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
     const int64_t groups = ao_group_count(n, c);
-    for (int64_t g = 0; g < groups; ++g) {
-        const int64_t off = ao_stripe_offset(g, c, n);
+    const int64_t rows_per_group = c->step * c->b_q;
+    int64_t* offs = (int64_t*)malloc((size_t)(groups + 1) * sizeof(int64_t));
+    int64_t* kept_n = (int64_t*)calloc((size_t)(groups > 0 ? groups : 1), sizeof(int64_t));
+    offs[0] = 0;
+    for (int64_t g = 0; g < groups; ++g) offs[g + 1] = offs[g] + middle_len(g, c, n);
+    for (int64_t g = 0; g < groups; ++g)
         for (int64_t s = 0; s < counts[g]; ++s)
-            if ((int64_t)idx[off + s] >= n) return -1;
-    }
+            if ((int64_t)idx[offs[g] + s] >= n) {
+                free(offs);
+                free(kept_n);
+                return -1;
+            }
     int64_t computed = ao_anchor_covered_count(n, c);
-#pragma omp parallel reduction(+ : computed)
+    for (int64_t g = 0; g < groups; ++g) {
+        const int64_t wstart = ao_window_start_token(g, c, n);
+        for (int64_t s = 0; s < counts[g]; ++s) {
+            const int64_t j = idx[offs[g] + s];
+            if (j >= c->b_kv && j < wstart) ++kept_n[g];
+        }
+        computed += kept_n[g] * (min64((g + 1) * rows_per_group, n) - g * rows_per_group);
+    }
+    const int64_t row_blocks = ceil_div(rows_per_group, ROWS);
+    const int64_t nsub = ceil_div(chunk, KT_W);
+#pragma omp parallel
     {
-        double* qk = (double*)malloc((size_t)chunk * sizeof(double));
-        uint32_t* kept = (uint32_t*)malloc((size_t)chunk * sizeof(uint32_t));
-        double* acc_row = (double*)malloc((size_t)d * sizeof(double));
-#pragma omp for schedule(dynamic, 16)
-        for (int64_t i = 0; i < n; ++i) {
-            const int64_t g = i / (c->step * c->b_q);
-            const int64_t off = ao_stripe_offset(g, c, n);
+        double* qk = (double*)malloc((size_t)(ROWS * nsub * KT_W) * sizeof(double));
+        double* kt = (double*)malloc((size_t)(KT_W * d) * sizeof(double));
+        int64_t* kept = (int64_t*)malloc((size_t)(nsub * KT_W) * sizeof(int64_t));
+        double* acc_rows = (double*)malloc((size_t)(ROWS * d) * sizeof(double));
+        double ms[ROWS], ls[ROWS];
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t w = 0; w < groups * row_blocks; ++w) {
+            const int64_t g = w / row_blocks;
+            const int64_t r0 = g * rows_per_group + (w % row_blocks) * ROWS;
+            const int64_t r1 = min64(min64(r0 + ROWS, (g + 1) * rows_per_group), n);
+            if (r0 >= r1) continue;
+            const int64_t nr = r1 - r0;
+            const int64_t off = offs[g];
             const int64_t cnt = counts[g];
             const int64_t wstart = ao_window_start_token(g, c, n);
-            double m = m_in[i], l = l_in[i];
-            memcpy(acc_row, acc_in + i * d, (size_t)d * sizeof(double));
-            const float* q_row = q + i * d;
+            for (int64_t r = 0; r < nr; ++r) {
+                ms[r] = m_in[r0 + r];
+                ls[r] = l_in[r0 + r];
+                memcpy(acc_rows + r * d, acc_in + (r0 + r) * d, (size_t)d * sizeof(double));
+            }
             for (int64_t c0 = 0; c0 < cnt; c0 += chunk) {
                 const int64_t c1 = min64(c0 + chunk, cnt);
                 int64_t taken = 0;
-                double chunk_max = -INFINITY;
                 for (int64_t s = c0; s < c1; ++s) {
                     const int64_t j = idx[off + s];
-                    if (j > i) continue;
                     if (j < c->b_kv || j >= wstart) continue;
-                    double sum = 0.0;
-                    const float* k_row = k + j * d;
-                    for (int64_t t = 0; t < d; ++t) sum += (double)q_row[t] * (double)k_row[t];
-                    qk[taken] = sum * inv_sqrt_d;
-                    if (qk[taken] > chunk_max) chunk_max = qk[taken];
-                    kept[taken] = (uint32_t)j;
-                    ++taken;
+                    kept[taken++] = j;
                 }
                 if (taken == 0) continue;
-                computed += taken;
-                const double m_new = m > chunk_max ? m : chunk_max;
-                const double alpha = exp(m - m_new);
-                for (int64_t t = 0; t < d; ++t) acc_row[t] *= alpha;
-                double l_chunk = 0.0;
-                for (int64_t s = 0; s < taken; ++s) {
-                    const double p = exp(qk[s] - m_new);
-                    l_chunk += p;
-                    const float* v_row = v + (int64_t)kept[s] * d;
-                    for (int64_t t = 0; t < d; ++t) acc_row[t] += p * (double)v_row[t];
+                for (int64_t sb = 0; sb * KT_W < taken; ++sb) {
+                    kt_load(k, d, kept + sb * KT_W, min64(KT_W, taken - sb * KT_W), kt);
+                    for (int64_t r = 0; r < nr; ++r)
+                        kt_dots(q + (r0 + r) * d, d, kt, qk + r * nsub * KT_W + sb * KT_W);
                 }
-                l = l * alpha + l_chunk;
-                m = m_new;
+                for (int64_t r = 0; r < nr; ++r) {
+                    double* qr = qk + r * nsub * KT_W;
+                    double* acc_row = acc_rows + r * d;
+                    double chunk_max = -INFINITY;
+                    for (int64_t s = 0; s < taken; ++s) {
+                        qr[s] = qr[s] * inv_sqrt_d;
+                        if (qr[s] > chunk_max) chunk_max = qr[s];
+                    }
+                    const double m_new = ms[r] > chunk_max ? ms[r] : chunk_max;
+                    const double alpha = exp(ms[r] - m_new);
+                    for (int64_t t = 0; t < d; ++t) acc_row[t] *= alpha;
+                    double l_chunk = 0.0;
+                    for (int64_t s = 0; s < taken; ++s) {
+                        const double p = exp(qr[s] - m_new);
+                        l_chunk += p;
+                        const float* v_row = v + kept[s] * d;
+                        for (int64_t t = 0; t < d; ++t) acc_row[t] += p * (double)v_row[t];
+                    }
+                    ls[r] = ls[r] * alpha + l_chunk;
+                    ms[r] = m_new;
+                }
             }
-            const double inv_l = 1.0 / l;
-            for (int64_t t = 0; t < d; ++t) out[i * d + t] = (float)(acc_row[t] * inv_l);
+            for (int64_t r = 0; r < nr; ++r) {
+                const double inv_l = 1.0 / ls[r];
+                for (int64_t t = 0; t < d; ++t)
+                    out[(r0 + r) * d + t] = (float)(acc_rows[r * d + t] * inv_l);
+            }
         }
         free(qk);
+        free(kt);
         free(kept);
-        free(acc_row);
+        free(acc_rows);
     }
+    free(offs);
+    free(kept_n);
     return computed;
 }
 
@@ -321,77 +405,107 @@ void ao_finalize(int64_t n, int64_t d, const double* l, const double* acc, float
     }
 }
 
+/* Causal logits of rows [r0, r1) against keys [0, r1 - 1], row r at
+ * logits[(r - r0) * n + j]: key sub-blocks transposed once per row block. */
+static void causal_logits(int64_t n, int64_t d, const float* q, const float* k, int64_t r0,
+                          int64_t r1, double inv_sqrt_d, double* kt, double* logits) {
+    double tmp[KT_W];
+    for (int64_t j0 = 0; j0 < r1; j0 += KT_W) {
+        const int64_t cnt = min64(KT_W, r1 - j0);
+        kt_load_range(k, d, j0, cnt, kt);
+        for (int64_t i = max64(r0, j0); i < r1; ++i) {
+            kt_dots(q + i * d, d, kt, tmp);
+            double* lr = logits + (i - r0) * n;
+            for (int64_t u = 0; u < cnt && j0 + u <= i; ++u) lr[j0 + u] = tmp[u] * inv_sqrt_d;
+        }
+    }
+}
+
 /* R/src/oracle.cpp:66-94 */
 void ao_dense_attention(int64_t n, int64_t d, const float* q, const float* k, const float* v,
                         float* out) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
+    const int64_t nblk = ceil_div(n, ROWS);
 #pragma omp parallel
     {
-        double* logits = (double*)malloc((size_t)n * sizeof(double));
+        double* logits = (double*)malloc((size_t)(ROWS * n) * sizeof(double));
+        double* kt = (double*)malloc((size_t)(KT_W * d) * sizeof(double));
         double* acc = (double*)malloc((size_t)d * sizeof(double));
-#pragma omp for schedule(dynamic, 16)
-        for (int64_t i = 0; i < n; ++i) {
-            double row_max = -INFINITY;
-            for (int64_t j = 0; j <= i; ++j) {
-                double sum = 0.0;
-                for (int64_t t = 0; t < d; ++t) sum += (double)q[i * d + t] * (double)k[j * d + t];
-                logits[j] = sum * inv_sqrt_d;
-                if (logits[j] > row_max) row_max = logits[j];
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int64_t r0 = (nblk - 1 - b) * ROWS, r1 = min64(r0 + ROWS, n);
+            causal_logits(n, d, q, k, r0, r1, inv_sqrt_d, kt, logits);
+            for (int64_t i = r0; i < r1; ++i) {
+                const double* lr = logits + (i - r0) * n;
+                double row_max = -INFINITY;
+                for (int64_t j = 0; j <= i; ++j)
+                    if (lr[j] > row_max) row_max = lr[j];
+                double denom = 0.0;
+                for (int64_t t = 0; t < d; ++t) acc[t] = 0.0;
+                for (int64_t j = 0; j <= i; ++j) {
+                    const double p = exp(lr[j] - row_max);
+                    denom += p;
+                    for (int64_t t = 0; t < d; ++t) acc[t] += p * v[j * d + t];
+                }
+                for (int64_t t = 0; t < d; ++t) out[i * d + t] = (float)(acc[t] / denom);
             }
-            double denom = 0.0;
-            for (int64_t t = 0; t < d; ++t) acc[t] = 0.0;
-            for (int64_t j = 0; j <= i; ++j) {
-                const double p = exp(logits[j] - row_max);
-                denom += p;
-                for (int64_t t = 0; t < d; ++t) acc[t] += p * v[j * d + t];
-            }
-            for (int64_t t = 0; t < d; ++t) out[i * d + t] = (float)(acc[t] / denom);
         }
         free(logits);
+        free(kt);
         free(acc);
     }
 }
 
 /* recall(union_mask(idx), dense_probs) — R/src/metrics.cpp:8-19 over the mask
  * of R/src/sparse_exec.cpp:135-153 and probabilities of R/src/oracle.cpp:38-64
- * (each probability rounded to f32 as dense_probs stores it). */
+ * (each probability rounded to f32 as dense_probs stores it).  The per-row
+ * captured masses are summed in row order. */
 double ao_union_recall(int64_t n, int64_t d, const float* q, const float* k, const ao_cfg* c,
                        const uint32_t* idx, const int64_t* counts) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
-    double captured = 0.0;
-#pragma omp parallel reduction(+ : captured)
+    const int64_t nblk = ceil_div(n, ROWS);
+    double* row_cap = (double*)malloc((size_t)n * sizeof(double));
+#pragma omp parallel
     {
-        double* logits = (double*)malloc((size_t)n * sizeof(double));
+        double* logits = (double*)malloc((size_t)(ROWS * n) * sizeof(double));
+        double* kt = (double*)malloc((size_t)(KT_W * d) * sizeof(double));
         unsigned char* sel = (unsigned char*)malloc((size_t)n);
-#pragma omp for schedule(dynamic, 16)
-        for (int64_t i = 0; i < n; ++i) {
-            double row_max = -INFINITY;
-            for (int64_t j = 0; j <= i; ++j) {
-                double sum = 0.0;
-                for (int64_t t = 0; t < d; ++t) sum += (double)q[i * d + t] * (double)k[j * d + t];
-                logits[j] = sum * inv_sqrt_d;
-                if (logits[j] > row_max) row_max = logits[j];
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int64_t r0 = (nblk - 1 - b) * ROWS, r1 = min64(r0 + ROWS, n);
+            causal_logits(n, d, q, k, r0, r1, inv_sqrt_d, kt, logits);
+            for (int64_t i = r0; i < r1; ++i) {
+                double* lr = logits + (i - r0) * n;
+                double row_max = -INFINITY;
+                for (int64_t j = 0; j <= i; ++j)
+                    if (lr[j] > row_max) row_max = lr[j];
+                double denom = 0.0;
+                for (int64_t j = 0; j <= i; ++j) {
+                    lr[j] = exp(lr[j] - row_max);
+                    denom += lr[j];
+                }
+                const int64_t g = i / (c->step * c->b_q);
+                const int64_t wstart = ao_window_start_token(g, c, n);
+                memset(sel, 0, (size_t)(i + 1));
+                for (int64_t j = 0; j < min64(c->b_kv, i + 1); ++j) sel[j] = 1;
+                for (int64_t j = wstart; j <= i; ++j) sel[j] = 1;
+                const int64_t off = ao_stripe_offset(g, c, n);
+                for (int64_t s = 0; s < counts[g]; ++s) {
+                    const int64_t j = idx[off + s];
+                    if (j <= i && j >= c->b_kv && j < wstart) sel[j] = 1;
+                }
+                double captured = 0.0;
+                for (int64_t j = 0; j <= i; ++j)
+                    if (sel[j]) captured += (double)(float)(lr[j] / denom);
+                row_cap[i] = captured;
             }
-            double denom = 0.0;
-            for (int64_t j = 0; j <= i; ++j) {
-                logits[j] = exp(logits[j] - row_max);
-                denom += logits[j];
-            }
-            const int64_t g = i / (c->step * c->b_q);
-            const int64_t wstart = ao_window_start_token(g, c, n);
-            memset(sel, 0, (size_t)(i + 1));
-            for (int64_t j = 0; j < min64(c->b_kv, i + 1); ++j) sel[j] = 1;
-            for (int64_t j = wstart; j <= i; ++j) sel[j] = 1;
-            const int64_t off = ao_stripe_offset(g, c, n);
-            for (int64_t s = 0; s < counts[g]; ++s) {
-                const int64_t j = idx[off + s];
-                if (j <= i && j >= c->b_kv && j < wstart) sel[j] = 1;
-            }
-            for (int64_t j = 0; j <= i; ++j)
-                if (sel[j]) captured += (double)(float)(logits[j] / denom);
         }
         free(logits);
+        free(kt);
         free(sel);
     }
+    double captured = 0.0;
+    for (int64_t i = 0; i < n; ++i) captured += row_cap[i];
+    free(row_cap);
     return captured / (double)n;
 }
