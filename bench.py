@@ -278,7 +278,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2505_23520_b200 import capi
-    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
+    from paper_2505_23520_b200.workloads import gen_layer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -317,15 +317,9 @@ def run_ours(args):
     # this rank's KV heads and their query heads (KV-head blocks, or with more
     # ranks than KV heads a run of one KV head's query heads); each KV head is
     # generated from its own seed so the data does not depend on the rank count
-    qs, ks, vs = [], [], []
-    for kvh in range(shard.kv_begin, shard.kv_end):
-        q, k, v = gen_sink_workload(SinkWorkloadSpec(n=args.n, hq=rep, hkv=1,
-                                                     seed=args.seed + kvh), device=dev)
-        lo = max(shard.q_begin - kvh * rep, 0)
-        hi = min(shard.q_end - kvh * rep, rep)
-        qs.append(q[lo:hi].contiguous()), ks.append(k), vs.append(v)
-    q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
-    del qs, ks, vs
+    q, k, v = gen_layer(args.n, args.hq, args.hkv, args.seed, device=dev,
+                        kv_heads=range(shard.kv_begin, shard.kv_end),
+                        q_range=(shard.q_begin, shard.q_end))
     cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
     pipe = capi.Pipeline(q, k, v, cfg)
     hq_local = q.shape[0]

@@ -133,15 +133,22 @@ aa_status aa_identify(const aa_problem* p, const void* k, const float* qbar,
                       aa_stream_t stream);
 
 /* Alg. 3 — sparse_attention (R/src/sparse_exec.cpp:13-124).  Resumes (m, l,
- * acc), folds each group's listed stripes, writes O = acc / l.  Index lists
- * must already be filtered to [b_kv, window_start(g)) (identify output always
- * is; the C++ shim filters user lists the way sparse_exec.cpp:79-82 skips).
+ * acc), folds each group's listed stripes, writes O = acc / l.
+ * offsets: NULL for the capacity layout, else a device CSR table
+ * [hq * groups + 1] of list starts (counts gives the lengths).  Lists may hold
+ * any indices, as the reference's StripeIndex may:
+ *   - an index >= n fails with AA_ERR_OUT_OF_RANGE and the reference's text
+ *     "sparse_attention: stripe index N out of range" (sparse_exec.cpp:51-56;
+ *     the first such index in (head, group, position) order);
+ *   - entries outside [b_kv, window_start(g)) (anchor-covered or non-causal)
+ *     are skipped and duplicates fold twice, as sparse_exec.cpp:79-82 does —
+ *     the exact path per row inside the reference's chunks; the fast path
+ *     compacts each list on the device first (order kept) and folds 128-key
+ *     tiles.
+ * The lists are validated on the device before any output is written, so
+ * this call synchronizes `stream` (the fused aa_anchor_attention does not).
  * fold_chunk is FoldPlan::index_chunk for the exact path (ignored by the fast
- * path, which folds 128-key tiles).  offsets: NULL for the capacity layout,
- * else a device CSR table [hq * groups + 1] of list starts (counts gives the
- * lengths); lists may then hold any indices, which are filtered per row exactly
- * as sparse_exec.cpp:79-82 (exact path) — the fast path requires filtered
- * lists.  computed may be NULL. */
+ * path).  computed may be NULL. */
 aa_status aa_sparse_attention(const aa_problem* p, const void* q, const void* k, const void* v,
                               const void* m, const void* l, const void* acc,
                               const uint32_t* indices, const int32_t* counts,
@@ -161,8 +168,11 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
 
 /* Same chain on HOST buffers (the reference's value-semantics calling
  * convention, bindings.cpp:21-32): copies q/k/v in, runs, copies out and the
- * per-head computed counts back; blocks until done.  Device buffers are
- * cached across calls of the same size.  The copies are pipelined against the
+ * per-head computed counts back; blocks until done.  Device buffers, streams
+ * and events are cached per device across calls (calls on one device are
+ * serialized; several devices may be driven from one process).  The bf16
+ * path fails with AA_ERR_UNSUPPORTED when V holds values outside the f16
+ * range (|v| > 65504, see below).  The copies are pipelined against the
  * chain over up to 32 chunks — blocks of KV heads, or runs of one KV head's
  * query heads when there are fewer KV heads than chunks — on copy-in, compute
  * and copy-out streams, so with page-locked host buffers the PCIe traffic
@@ -170,6 +180,13 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
 aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const void* k,
                                    const void* v, int zero_anchor, void* out, aa_dtype out_dtype,
                                    int64_t* computed);
+
+/* Numerical range of the bf16 (tcgen05) path: PV runs in f16 (V converted
+ * bf16 -> f16 once, exact for 6.1e-5 <= |v| <= 65504; smaller magnitudes lose
+ * relative, not absolute, precision) and the fused chain hands K1's state to
+ * K3 as f16 acc / l (|.| <= max |v|).  V outside that range gives non-finite
+ * outputs; aa_anchor_attention_host detects it, the device-buffer entries do
+ * not check (use AA_F32 for such data). */
 
 /* Dense causal attention (oracle.cpp:66-94 semantics) — the baseline the
  * sparse path is measured against (exact path: f64; fast path: tcgen05). */

@@ -268,21 +268,18 @@ void ao_identify(int64_t n, int64_t d, const float* q, const float* k, const dou
  * and its keys transposed once per block of ROWS rows. */
 #define ROWS 16
 
-int64_t ao_sparse_attention(int64_t n, int64_t d, const float* q, const float* k, const float* v,
-                            const ao_cfg* c, const double* m_in, const double* l_in,
-                            const double* acc_in, const uint32_t* idx, const int64_t* counts,
-                            int64_t chunk, float* out) {
+/* Group g's list is idx[offs[g] .. offs[g] + counts[g]). */
+static int64_t sparse_core(int64_t n, int64_t d, const float* q, const float* k, const float* v,
+                           const ao_cfg* c, const double* m_in, const double* l_in,
+                           const double* acc_in, const uint32_t* idx, const int64_t* offs,
+                           const int64_t* counts, int64_t chunk, float* out) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
     const int64_t groups = ao_group_count(n, c);
     const int64_t rows_per_group = c->step * c->b_q;
-    int64_t* offs = (int64_t*)malloc((size_t)(groups + 1) * sizeof(int64_t));
     int64_t* kept_n = (int64_t*)calloc((size_t)(groups > 0 ? groups : 1), sizeof(int64_t));
-    offs[0] = 0;
-    for (int64_t g = 0; g < groups; ++g) offs[g + 1] = offs[g] + middle_len(g, c, n);
     for (int64_t g = 0; g < groups; ++g)
         for (int64_t s = 0; s < counts[g]; ++s)
             if ((int64_t)idx[offs[g] + s] >= n) {
-                free(offs);
                 free(kept_n);
                 return -1;
             }
@@ -366,9 +363,29 @@ int64_t ao_sparse_attention(int64_t n, int64_t d, const float* q, const float* k
         free(kept);
         free(acc_rows);
     }
-    free(offs);
     free(kept_n);
     return computed;
+}
+
+int64_t ao_sparse_attention(int64_t n, int64_t d, const float* q, const float* k, const float* v,
+                            const ao_cfg* c, const double* m_in, const double* l_in,
+                            const double* acc_in, const uint32_t* idx, const int64_t* counts,
+                            int64_t chunk, float* out) {
+    const int64_t groups = ao_group_count(n, c);
+    int64_t* offs = (int64_t*)malloc((size_t)(groups + 1) * sizeof(int64_t));
+    offs[0] = 0;
+    for (int64_t g = 0; g < groups; ++g) offs[g + 1] = offs[g] + middle_len(g, c, n);
+    const int64_t r = sparse_core(n, d, q, k, v, c, m_in, l_in, acc_in, idx, offs, counts, chunk, out);
+    free(offs);
+    return r;
+}
+
+int64_t ao_sparse_attention_lists(int64_t n, int64_t d, const float* q, const float* k,
+                                  const float* v, const ao_cfg* c, const double* m_in,
+                                  const double* l_in, const double* acc_in, const uint32_t* idx,
+                                  const int64_t* starts, const int64_t* counts, int64_t chunk,
+                                  float* out) {
+    return sparse_core(n, d, q, k, v, c, m_in, l_in, acc_in, idx, starts, counts, chunk, out);
 }
 
 /* R/src/sparse_exec.cpp:126-133 (+ pooled_anchor, stripe_identify.cpp:71-74). */

@@ -67,6 +67,14 @@ int64_t ao_sparse_attention(int64_t n, int64_t d, const float* q, const float* k
                             const double* acc, const uint32_t* idx, const int64_t* counts,
                             int64_t chunk, float* out);
 
+/* Same over arbitrary per-group lists (a StripeIndex of any lengths): group
+ * g's list is idx[starts[g] .. starts[g] + counts[g]). */
+int64_t ao_sparse_attention_lists(int64_t n, int64_t d, const float* q, const float* k,
+                                  const float* v, const ao_cfg* cfg, const double* m,
+                                  const double* l, const double* acc, const uint32_t* idx,
+                                  const int64_t* starts, const int64_t* counts, int64_t chunk,
+                                  float* out);
+
 /* anchor_attention (sparse_exec.cpp:126-133): the whole chain. Returns
  * computed_positions.  If state/idx buffers are non-NULL they are filled. */
 int64_t ao_anchor_attention(int64_t n, int64_t d, const float* q, const float* k,

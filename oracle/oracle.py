@@ -96,6 +96,9 @@ class Oracle:
         L.ao_sparse_attention.restype = _i64
         L.ao_sparse_attention.argtypes = [_i64, _i64, _p, _p, _p, C.POINTER(_Cfg), _p, _p, _p,
                                           _p, _p, _i64, _p]
+        L.ao_sparse_attention_lists.restype = _i64
+        L.ao_sparse_attention_lists.argtypes = [_i64, _i64, _p, _p, _p, C.POINTER(_Cfg), _p, _p,
+                                                _p, _p, _p, _p, _i64, _p]
         L.ao_anchor_attention.restype = _i64
         L.ao_anchor_attention.argtypes = [_i64, _i64, _p, _p, _p, C.POINTER(_Cfg), C.c_int, _p,
                                           _p, _p, _p, _p]
@@ -197,6 +200,28 @@ class Oracle:
         computed = self.L.ao_sparse_attention(n, d, _ptr(q), _ptr(k), _ptr(v), C.byref(c),
                                               _ptr(m), _ptr(l), _ptr(acc), _ptr(idx),
                                               _ptr(counts), chunk, _ptr(out))
+        if computed < 0:
+            raise IndexError("sparse_attention: stripe index out of range")
+        return out, int(computed)
+
+    def sparse_lists(self, q, k, v, cfg, m, l, acc, lists, chunk=64):
+        """sparse_attention over a StripeIndex given as per-group lists of any
+        length and content (the reference filters them per row)."""
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        n, d = q.shape
+        starts = np.zeros(len(lists), np.int64)
+        counts = np.array([len(x) for x in lists], np.int64)
+        if len(lists):
+            starts[1:] = np.cumsum(counts)[:-1]
+        flat = np.zeros(max(int(counts.sum()), 1), np.uint32)
+        for s0, x in zip(starts, lists):
+            flat[s0:s0 + len(x)] = np.asarray(x, dtype=np.uint64).astype(np.uint32)
+        out = np.empty((n, d), np.float32)
+        c = cfg.c()
+        computed = self.L.ao_sparse_attention_lists(
+            n, d, _ptr(q), _ptr(k), _ptr(v), C.byref(c), _ptr(np.ascontiguousarray(m, np.float64)),
+            _ptr(np.ascontiguousarray(l, np.float64)), _ptr(np.ascontiguousarray(acc, np.float64)),
+            _ptr(flat), _ptr(starts), _ptr(counts), chunk, _ptr(out))
         if computed < 0:
             raise IndexError("sparse_attention: stripe index out of range")
         return out, int(computed)

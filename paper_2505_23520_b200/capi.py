@@ -138,7 +138,13 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise TypeError(f"q/k/v must be bfloat16 (fast path) or float32 (exact path), got {t.dtype}")
 
 
-def make_problem(q: torch.Tensor, k: torch.Tensor, cfg: BlockConfig) -> _Problem:
+def make_problem(q: torch.Tensor, k: torch.Tensor, cfg: BlockConfig,
+                 v: torch.Tensor | None = None) -> _Problem:
+    """The C-ABI problem for q [hq, n, d] and k (and v) [hkv, n, d].
+
+    The ABI reads v with k's strides and q's dtype, so v (when given) must
+    match k in shape, strides, dtype and device, and k must share q's dtype
+    and device."""
     if q.dim() != 3 or k.dim() != 3:
         raise ValueError("expected q [hq, n, d] and k/v [hkv, n, d]")
     hq, n, d = q.shape
@@ -147,8 +153,32 @@ def make_problem(q: torch.Tensor, k: torch.Tensor, cfg: BlockConfig) -> _Problem
         raise ValueError("q and k/v must share (n, d)")
     if q.stride(2) != 1 or k.stride(2) != 1:
         raise ValueError("head dim must be contiguous")
+    if k.dtype != q.dtype:
+        raise TypeError(f"q and k must share a dtype, got {q.dtype} and {k.dtype}")
+    if k.device != q.device:
+        raise ValueError("q and k must be on the same device")
+    if v is not None:
+        if v.shape != k.shape:
+            raise ValueError(f"v shape {tuple(v.shape)} != k shape {tuple(k.shape)}")
+        if v.dtype != k.dtype:
+            raise TypeError(f"v dtype {v.dtype} != k dtype {k.dtype}")
+        if v.device != k.device:
+            raise ValueError("v must be on k's device")
+        if v.stride() != k.stride():
+            raise ValueError(f"v strides {v.stride()} != k strides {k.stride()} (the ABI reads "
+                             "v with k's kv strides)")
     return _Problem(n, d, hq, hkv, cfg.c(), _dtype_code(q), q.stride(1), q.stride(0),
                     k.stride(1), k.stride(0))
+
+
+def _same_layout(p: _Problem, q, k, v) -> None:
+    """Re-check tensors handed to a Pipeline built for problem ``p``."""
+    p2 = make_problem(q, k, BlockConfig(p.cfg.b_q, p.cfg.b_kv, p.cfg.step, p.cfg.theta), v)
+    for f in ("n", "d", "hq", "hkv", "dtype", "q_row_stride", "q_head_stride", "kv_row_stride",
+              "kv_head_stride"):
+        if getattr(p2, f) != getattr(p, f):
+            raise ValueError(f"tensors do not match the Pipeline's problem ({f}: "
+                             f"{getattr(p2, f)} != {getattr(p, f)})")
 
 
 def plan(p: _Problem) -> _Plan:
@@ -172,15 +202,18 @@ class Pipeline:
 
     def __init__(self, q, k, v, cfg: BlockConfig):
         self.cfg = cfg
-        self.p = make_problem(q, k, cfg)
+        self.p = make_problem(q, k, cfg, v)
         self.plan = plan(self.p)
         self.workspace = torch.empty(self.plan.workspace_bytes, dtype=torch.uint8, device=q.device)
 
     def __call__(self, q, k, v, zero_anchor=False, out=None, out_dtype=torch.float32,
                  computed=None):
+        _same_layout(self.p, q, k, v)
         hq, n, d = q.shape
         if out is None:
             out = torch.empty((hq, n, d), dtype=out_dtype, device=q.device)
+        elif out.shape != q.shape or not out.is_contiguous() or out.device != q.device:
+            raise ValueError("out must be a contiguous [hq, n, d] tensor on q's device")
         if computed is None:
             computed = torch.empty(hq, dtype=torch.int64, device=q.device)
         _check(lib().aa_anchor_attention(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v),
@@ -241,7 +274,7 @@ def anchor_attention(q, k, v, cfg=BlockConfig(), zero_anchor=False, out_dtype=to
 
 def compute_anchor(q, k, v, cfg=BlockConfig()):
     """Alg. 1: returns dict(m, l, acc, qsum, msum) (state f64 on the exact path)."""
-    p = make_problem(q, k, cfg)
+    p = make_problem(q, k, cfg, v)
     pl = plan(p)
     hq, n, d = q.shape
     sdt = torch.float64 if pl.state_dtype == AA_F64 else torch.float32
@@ -294,7 +327,7 @@ def identify(q, k, qbar, anchor, cfg=BlockConfig(), zero_anchor=False, out=None,
 def sparse(q, k, v, state, idx, counts, cfg=BlockConfig(), offsets=None, fold_chunk=64,
            out_dtype=torch.float32):
     """Alg. 3: returns (out [hq, n, d], computed [hq])."""
-    p = make_problem(q, k, cfg)
+    p = make_problem(q, k, cfg, v)
     hq, n, d = q.shape
     out = torch.empty((hq, n, d), dtype=out_dtype, device=q.device)
     computed = torch.empty(hq, dtype=torch.int64, device=q.device)
@@ -315,7 +348,7 @@ def finalize(q, k, state, cfg=BlockConfig(), out_dtype=torch.float32):
 
 def dense_attention(q, k, v, out_dtype=torch.float32, out=None):
     """Dense causal attention (the baseline; exact or tcgen05 by dtype)."""
-    p = make_problem(q, k, BlockConfig())
+    p = make_problem(q, k, BlockConfig(), v)
     if out is None:
         out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
     _check(lib().aa_dense_attention(C.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
@@ -345,7 +378,10 @@ def dense_tile_mass(q, k, cfg=BlockConfig()):
 def anchor_attention_host(q, k, v, cfg=BlockConfig(), zero_anchor=False,
                           out_dtype=torch.float32, out=None, computed=None):
     """The chain on HOST (pinned) tensors through aa_anchor_attention_host."""
-    p = make_problem(q, k, cfg)
+    p = make_problem(q, k, cfg, v)
+    for t in (q, k, v):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("anchor_attention_host takes contiguous host tensors")
     if out is None:
         out = torch.empty(q.shape, dtype=out_dtype, pin_memory=q.is_pinned())
     out_dtype = out.dtype

@@ -73,7 +73,7 @@ struct Carve {
 
 struct Layout {
     void *m, *l, *acc, *qsum, *msum, *anchor, *qbar, *offsets, *bits, *indices, *counts, *taken,
-        *v16, *split;
+        *v16, *split, *flags;
     size_t split_bytes;
     int64_t words_per_row;
     size_t total;
@@ -104,6 +104,7 @@ Layout carve(const aa_problem& p, const aa_plan& plan, void* ws) {
     // K2's split A operand (q_bar = hi + lo, bf16) of the fast path
     L.split_bytes = p.dtype == AA_BF16 ? aa::fast_identify_scratch_bytes(fast_args(p)) : 0;
     L.split = L.split_bytes ? c.take(L.split_bytes) : nullptr;
+    L.flags = c.take(8);  // fast path: count of V values outside the f16 range
     L.total = c.off;
     return L;
 }
@@ -397,28 +398,73 @@ aa_status aa_sparse_attention(const aa_problem* p, const void* q, const void* k,
     if (aa_status s = require_device()) return s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const aa::Geo G = geo_of(p->n, p->cfg);
+    const int64_t groups = plan.groups, rows = p->hq * groups;
     const int64_t cap = plan.stripe_capacity > 0 ? plan.stripe_capacity : 1;
-    Temp tmp(st);
-    AA_CUDA(tmp.alloc(align256(static_cast<size_t>(plan.groups + 1) * 8) +
-                      static_cast<size_t>(p->hq) * 8));
-    int64_t* offs = static_cast<int64_t*>(tmp.p);
-    unsigned long long* taken = reinterpret_cast<unsigned long long*>(
-        static_cast<char*>(tmp.p) + align256(static_cast<size_t>(plan.groups + 1) * 8));
-    // CSR tables index [h * groups + g] directly; the capacity layout adds h * cap.
-    int64_t row_cap = cap;
-    if (offsets) {
-        row_cap = 0;
-    } else {
-        AA_CUDA(aa::launch_offsets(G, offs, st));
+    const bool fast = p->dtype == AA_BF16;
+    // The caller's lists are checked on the device first (R/src/sparse_exec.cpp:51-56:
+    // an index >= n is std::out_of_range, reported for the first one in
+    // (head, group, position) order); the fast path then folds 128-key tiles
+    // of the entries the reference folds (:79-82), compacted per list.
+    std::vector<int32_t> hcounts(static_cast<size_t>(rows));
+    if (rows > 0)
+        AA_CUDA(cudaMemcpyAsync(hcounts.data(), counts, hcounts.size() * 4, cudaMemcpyDeviceToHost, st));
+    AA_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> hoff(static_cast<size_t>(rows) + 1, 0);
+    int64_t max_count = 1;
+    for (int64_t r = 0; r < rows; ++r) {
+        max_count = std::max<int64_t>(max_count, hcounts[r]);
+        if (hcounts[r] < 0)
+            return fail(AA_ERR_INVALID_ARGUMENT, "sparse_attention: negative stripe count");
+        hoff[r + 1] = hoff[r] + hcounts[r];
     }
+    const size_t off_b = align256(static_cast<size_t>(groups + 1) * 8);
+    const size_t coff_b = align256(hoff.size() * 8);
+    const size_t cnt_b = align256(static_cast<size_t>(rows) * 4 + 4);
+    const size_t idx_b = fast ? align256(static_cast<size_t>(hoff[rows]) * 4 + 4) : 0;
+    Temp tmp(st);
+    AA_CUDA(tmp.alloc(off_b + coff_b + cnt_b + idx_b + align256(static_cast<size_t>(p->hq) * 8) + 256));
+    char* base = static_cast<char*>(tmp.p);
+    int64_t* offs = reinterpret_cast<int64_t*>(base);
+    int64_t* coff = reinterpret_cast<int64_t*>(base + off_b);
+    int32_t* fcounts = reinterpret_cast<int32_t*>(base + off_b + coff_b);
+    uint32_t* fidx = fast ? reinterpret_cast<uint32_t*>(base + off_b + coff_b + cnt_b) : nullptr;
+    unsigned long long* taken =
+        reinterpret_cast<unsigned long long*>(base + off_b + coff_b + cnt_b + idx_b);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(
+        base + off_b + coff_b + cnt_b + idx_b + align256(static_cast<size_t>(p->hq) * 8));
+    if (!offsets) AA_CUDA(aa::launch_offsets(G, offs, st));
     const int64_t* offs_used = offsets ? offsets : offs;
-    if (p->dtype == AA_F32) {
+    AA_CUDA(cudaMemcpyAsync(coff, hoff.data(), hoff.size() * 8, cudaMemcpyHostToDevice, st));
+    AA_CUDA(cudaMemsetAsync(bad, 0xff, 8, st));
+    AA_CUDA(aa::launch_filter_lists(G, p->hq, indices, counts, offs_used, cap, offsets != nullptr,
+                                    coff, fidx, fast ? fcounts : nullptr, bad, st));
+    unsigned long long hbad = 0;
+    AA_CUDA(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st));
+    AA_CUDA(cudaStreamSynchronize(st));
+    if (hbad != ~0ull) {
+        const int64_t row = static_cast<int64_t>(hbad >> 32), pos = static_cast<int64_t>(hbad & 0xffffffffull);
+        const int64_t h = row / groups, g = row % groups;
+        int64_t start = 0;
+        if (offsets) {
+            AA_CUDA(cudaMemcpy(&start, offsets + row, 8, cudaMemcpyDeviceToHost));
+        } else {
+            start = h * cap + G.stripe_offset(g);
+        }
+        uint32_t j = 0;
+        AA_CUDA(cudaMemcpy(&j, indices + start + pos, 4, cudaMemcpyDeviceToHost));
+        return fail(AA_ERR_OUT_OF_RANGE,
+                    "sparse_attention: stripe index " + std::to_string(j) + " out of range");
+    }
+    if (!fast) {
         AA_CUDA(cudaMemsetAsync(taken, 0, static_cast<size_t>(p->hq) * 8, st));
         AA_CUDA(aa::launch_sparse_exact(
             exact_args(*p), static_cast<const float*>(q), static_cast<const float*>(k),
             static_cast<const float*>(v), static_cast<const double*>(m),
             static_cast<const double*>(l), static_cast<const double*>(acc), indices, counts,
-            offs_used, row_cap, offsets != nullptr, fold_chunk, out, out_dtype, taken, st));
+            offs_used, offsets ? 0 : cap, offsets != nullptr,
+            // a chunk longer than every list folds each list in one chunk,
+            // exactly as the requested chunk does (it bounds shared memory)
+            std::min(fold_chunk, max_count), out, out_dtype, taken, st));
         if (computed)
             AA_CUDA(aa::launch_add_u64(p->hq, plan.covered_positions, taken, computed, st));
     } else {
@@ -427,11 +473,10 @@ aa_status aa_sparse_attention(const aa_problem* p, const void* q, const void* k,
         AA_CUDA(v16.alloc(static_cast<size_t>(p->hkv * p->n * p->d) * 2));
         AA_CUDA(aa::fast_convert_v(f, v, v16.p, st));
         AA_CUDA(aa::fast_sparse(f, q, k, v16.p, static_cast<const float*>(m),
-                                static_cast<const float*>(l), static_cast<const float*>(acc),
-                                indices, counts, offs_used, row_cap, offsets != nullptr, out,
-                                out_dtype, st));
+                                static_cast<const float*>(l), static_cast<const float*>(acc), fidx,
+                                fcounts, coff, 0, true, out, out_dtype, st));
         if (computed)
-            AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions, counts, computed, st));
+            AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions, fcounts, computed, st));
     }
     return AA_OK;
 }
@@ -502,7 +547,8 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
     }
     const aa::FastArgs f = fast_args(*p);
     mark(0, st);
-    AA_CUDA(aa::fast_convert_v(f, v, L.v16, st));
+    AA_CUDA(cudaMemsetAsync(L.flags, 0, 8, st));
+    AA_CUDA(aa::fast_convert_v(f, v, L.v16, st, static_cast<unsigned*>(L.flags)));
     mark(1, st);
     AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
                             static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
@@ -557,13 +603,31 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     // chunk c's inputs go up on the copy-in stream while chunk c-1 computes and
     // chunk c-2's output comes back on the copy-out stream, so the PCIe
     // transfers (both directions at once) hide the chain instead of adding to it.
-    static std::mutex mu;
-    static void* dbuf = nullptr;
-    static size_t dbytes = 0;
-    static cudaStream_t st_in = nullptr, st_c = nullptr, st_out = nullptr;
+    // Cached per device (streams, events and buffers belong to one device
+    // context; a process may drive several GPUs one after another).
     constexpr int kMaxChunks = 32;
-    static cudaEvent_t ev_in[kMaxChunks], ev_done[kMaxChunks];
-    std::lock_guard<std::mutex> lock(mu);
+    constexpr int kMaxDevices = 64;
+    struct DeviceState {
+        std::mutex mu;
+        void* dbuf = nullptr;
+        size_t dbytes = 0;
+        cudaStream_t st_in = nullptr, st_c = nullptr, st_out = nullptr;
+        cudaEvent_t ev_in[kMaxChunks], ev_done[kMaxChunks];
+        unsigned* v_flags = nullptr;  // pinned: per-chunk V-range counts
+    };
+    static DeviceState states[kMaxDevices];
+    int dev_id = 0;
+    if (aa_status s = require_device()) return s;
+    AA_CUDA(cudaGetDevice(&dev_id));
+    if (dev_id < 0 || dev_id >= kMaxDevices)
+        return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_host: device ordinal >= 64");
+    DeviceState& ds = states[dev_id];
+    std::lock_guard<std::mutex> lock(ds.mu);
+    void*& dbuf = ds.dbuf;
+    size_t& dbytes = ds.dbytes;
+    cudaStream_t &st_in = ds.st_in, &st_c = ds.st_c, &st_out = ds.st_out;
+    cudaEvent_t* ev_in = ds.ev_in;
+    cudaEvent_t* ev_done = ds.ev_done;
     aa_plan plan;
     if (aa_status s = aa_make_plan(p, &plan)) return s;
     if (out_dtype != AA_F32 && out_dtype != AA_BF16)
@@ -572,7 +636,6 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     if (!packed(p->q_row_stride, p->d) || !packed(p->q_head_stride, p->n * p->d) ||
         !packed(p->kv_row_stride, p->d) || !packed(p->kv_head_stride, p->n * p->d))
         return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_host: packed layouts only");
-    if (aa_status s = require_device()) return s;
     if (!st_c) {
         AA_CUDA(cudaStreamCreateWithFlags(&st_in, cudaStreamNonBlocking));
         AA_CUDA(cudaStreamCreateWithFlags(&st_c, cudaStreamNonBlocking));
@@ -581,6 +644,8 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
             AA_CUDA(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
             AA_CUDA(cudaEventCreateWithFlags(&ev_done[c], cudaEventDisableTiming));
         }
+        AA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ds.v_flags), kMaxChunks * sizeof(unsigned),
+                              cudaHostAllocDefault));
     }
     const int64_t rep = p->hkv > 0 ? p->hq / p->hkv : 1;
     // Chunks: blocks of whole KV heads, or — with fewer KV heads than chunks
@@ -650,6 +715,8 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     const char* hk_ = static_cast<const char*>(k);
     const char* hv_ = static_cast<const char*>(v);
     char* ho_ = static_cast<char*>(out);
+    unsigned* v_flags = ds.v_flags;
+    for (int c = 0; c < nchunks; ++c) v_flags[c] = 0;
     for (int c = 0; c < nchunks; ++c) {
         const int64_t kv0 = chunks[c].kv0, nkv = chunks[c].nkv, h0 = chunks[c].h0, nh = chunks[c].nh;
         const size_t qo = static_cast<size_t>(h0) * head_in, qn = static_cast<size_t>(nh) * head_in;
@@ -672,6 +739,11 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
             cudaStreamSynchronize(st_out);
             return s;
         }
+        if (p->dtype == AA_BF16) {
+            // the chunk's V-range count (workspace flags), summed on the host
+            const Layout WL = carve(sub, sub_plan, ws);
+            AA_CUDA(cudaMemcpyAsync(&v_flags[c], WL.flags, 4, cudaMemcpyDeviceToHost, st_c));
+        }
         AA_CUDA(cudaEventRecord(ev_done[c], st_c));
         AA_CUDA(cudaStreamWaitEvent(st_out, ev_done[c], 0));
         const size_t oo = static_cast<size_t>(h0) * head_out, on = static_cast<size_t>(nh) * head_out;
@@ -682,6 +754,12 @@ aa_status aa_anchor_attention_host(const aa_problem* p, const void* q, const voi
     AA_CUDA(cudaStreamSynchronize(st_in));
     AA_CUDA(cudaStreamSynchronize(st_c));
     AA_CUDA(cudaStreamSynchronize(st_out));
+    unsigned v_overflow = 0;
+    for (int c = 0; c < nchunks; ++c) v_overflow += v_flags[c];
+    if (p->dtype == AA_BF16 && v_overflow != 0)
+        return fail(AA_ERR_UNSUPPORTED,
+                    "aa_anchor_attention_host: |v| > 65504 does not fit the f16 PV operand of "
+                    "the bf16 path (output is not finite); use the exact path (AA_F32)");
     return AA_OK;
 }
 

@@ -146,7 +146,69 @@ __global__ void __launch_bounds__(1024) k_offsets(Geo geo, int64_t* __restrict__
     if (t == 0) offsets[0] = 0;
 }
 
+// Caller-supplied stripe lists of the stage API (capacity layout, or a CSR
+// table of list starts) -> the entries sparse_exec.cpp folds
+// (b_kv <= j < window_start(g), R/src/sparse_exec.cpp:79-82; window_start(g)
+// <= row_begin(g) whenever that range is non-empty, so the causal clamp
+// never fires on them), in list order, duplicates kept, written to
+// out_idx + out_off[h * G + g] (out_idx may be NULL: validation only).  The
+// first out-of-range entry j >= n in (head, group, position) order — the one
+// R/src/sparse_exec.cpp:51-56 reports — is recorded as the key
+// ((h * G + g) << 32 | position) in *first_bad (atomicMin).  grid (G, hq).
+__global__ void __launch_bounds__(256)
+    k_filter_lists(Geo geo, const uint32_t* __restrict__ idx, const int32_t* __restrict__ counts,
+                   const int64_t* __restrict__ offsets, int64_t cap, int csr,
+                   const int64_t* __restrict__ out_off, uint32_t* __restrict__ out_idx,
+                   int32_t* __restrict__ out_counts, unsigned long long* __restrict__ first_bad) {
+    __shared__ int warp_tot[8];
+    const int64_t G = geo.groups();
+    const int64_t g = blockIdx.x, h = blockIdx.y, row = h * G + g;
+    const int64_t cnt = counts[row];
+    const uint32_t* src = idx + (csr ? offsets[row] : h * cap + offsets[g]);
+    uint32_t* dst = out_idx ? out_idx + out_off[row] : nullptr;
+    const int64_t lo = geo.b_kv, hi = geo.window_start(g), n = geo.n;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t base = 0;
+    for (int64_t b = 0; b < cnt; b += 256) {
+        const int64_t e = b + threadIdx.x;
+        uint32_t j = 0;
+        bool keep = false;
+        if (e < cnt) {
+            j = src[e];
+            if (j >= n)
+                atomicMin(first_bad, (static_cast<unsigned long long>(row) << 32) |
+                                         static_cast<unsigned long long>(e));
+            keep = j >= lo && j < hi;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) warp_tot[wid] = __popc(bal);
+        __syncthreads();
+        int pre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            pre += w < wid ? warp_tot[w] : 0;
+            tot += warp_tot[w];
+        }
+        if (keep && dst) dst[base + pre + __popc(bal & ((1u << lane) - 1u))] = j;
+        base += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && out_counts) out_counts[row] = static_cast<int32_t>(base);
+}
+
 }  // namespace
+
+cudaError_t launch_filter_lists(const Geo& geo, int64_t hq, const uint32_t* idx,
+                                const int32_t* counts, const int64_t* offsets, int64_t cap,
+                                bool csr, const int64_t* out_off, uint32_t* out_idx,
+                                int32_t* out_counts, unsigned long long* first_bad,
+                                cudaStream_t s) {
+    const int64_t G = geo.groups();
+    if (G == 0 || hq == 0) return cudaSuccess;
+    k_filter_lists<<<dim3(static_cast<unsigned>(G), static_cast<unsigned>(hq)), 256, 0, s>>>(
+        geo, idx, counts, offsets, cap, csr ? 1 : 0, out_off, out_idx, out_counts, first_bad);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_offsets(const Geo& geo, int64_t* offsets, cudaStream_t s) {
     k_offsets<<<1, 1024, 0, s>>>(geo, offsets);

@@ -360,8 +360,9 @@ cudaError_t launch_anchor_exact(const ExactArgs& a, const float* q, const float*
                                 cudaStream_t s) {
     const size_t smem = static_cast<size_t>(a.geo.b_kv + a.d) * sizeof(double);
     if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_anchor_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        const cudaError_t e = cudaFuncSetAttribute(
+            k_anchor_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
     }
     k_anchor_exact<<<dim3(static_cast<unsigned>(a.geo.n), static_cast<unsigned>(a.hq)), 32, smem,
                      s>>>(a, q, k, v, m, l, acc);
@@ -391,8 +392,11 @@ cudaError_t launch_sparse_exact(const ExactArgs& a, const float* q, const float*
                                 cudaStream_t s) {
     const size_t smem = static_cast<size_t>(a.d) * 8 + static_cast<size_t>(chunk) * 12;
     if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_sparse_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        // beyond 227 KB (index_chunk above ~19k with lists that long) the
+        // launch is refused with the attribute's error
+        const cudaError_t e = cudaFuncSetAttribute(
+            k_sparse_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
     }
     k_sparse_exact<<<dim3(static_cast<unsigned>(a.geo.n), static_cast<unsigned>(a.hq)), 32, smem,
                      s>>>(a, q, k, v, m, l, acc, indices, counts, offsets, cap, csr, chunk, out,
@@ -411,8 +415,9 @@ cudaError_t launch_dense_exact(const ExactArgs& a, const float* q, const float* 
                                const float* v, void* out, aa_dtype out_dtype, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(a.d + 32) * sizeof(double);
     if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_dense_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        const cudaError_t e = cudaFuncSetAttribute(
+            k_dense_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
     }
     k_dense_exact<<<dim3(static_cast<unsigned>(a.geo.n), static_cast<unsigned>(a.hq)), 32, smem,
                     s>>>(a, q, k, v, out, out_dtype);

@@ -20,8 +20,10 @@ struct FastArgs {
 // Records stage event i of aa_set_stage_events on `st` (no-op when unset).
 void stage_mark(int i, cudaStream_t st);
 
-// V (bf16, strided) -> packed f16 copy [hkv, n, d] consumed by the PV MMAs.
-cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s);
+// V (bf16, strided) -> packed f16 copy [hkv, n, d] consumed by the PV MMAs;
+// values outside the f16 range are counted into *overflow (may be NULL).
+cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s,
+                           unsigned* overflow = nullptr);
 // K1 — Alg. 1 anchor pass (tile list {0} ∪ [wsb(g), qb]); writes f32 m, l,
 // acc and the per-q-block partial sums qsum [hq, T_m, d] / msum [hq, T_m].
 // acc_f16: acc is written as f16 acc / l (the fused chain's hand-off to K3,

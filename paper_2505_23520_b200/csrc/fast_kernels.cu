@@ -1331,10 +1331,14 @@ __global__ void k_recall_sum(int64_t n, const double* __restrict__ rows, double*
     if (threadIdx.x == 0) recall[h] = red[0] / static_cast<double>(n);
 }
 
-// V (bf16, strided) -> packed f16 [hkv, n, d] (exact for the f16 normal range).
+// V (bf16, strided) -> packed f16 [hkv, n, d] (exact for the f16 normal
+// range).  |v| > 65504 (or a non-finite v) does not fit f16: such values are
+// counted into *overflow when it is given (the host entry reports them).
 __global__ void k_v_to_f16(int64_t n, int64_t hkv, int64_t rs, int64_t hs,
-                           const __nv_bfloat16* __restrict__ v, __half* __restrict__ v16) {
+                           const __nv_bfloat16* __restrict__ v, __half* __restrict__ v16,
+                           unsigned* __restrict__ overflow) {
     const int64_t total8 = hkv * n * (kD / 8);
+    bool bad = false;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total8;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t hh = e / (n * (kD / 8));
@@ -1345,9 +1349,15 @@ __global__ void k_v_to_f16(int64_t n, int64_t hkv, int64_t rs, int64_t hs,
         uint4 o;
         __half2* o2 = reinterpret_cast<__half2*>(&o);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) o2[u] = __float22half2_rn(__bfloat1622float2(b2[u]));
+        for (int u = 0; u < 4; ++u) {
+            const float2 x = __bfloat1622float2(b2[u]);
+            bad |= !(fabsf(x.x) <= 65504.f) || !(fabsf(x.y) <= 65504.f);
+            o2[u] = __float22half2_rn(x);
+        }
         *reinterpret_cast<uint4*>(v16 + (hh * n + i) * kD + c8 * 8) = o;
     }
+    if (overflow != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicAdd(overflow, 1u);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1418,6 +1428,20 @@ cudaError_t make_map_gather(CUtensorMap* m, const void* base, CUtensorMapDataTyp
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Dynamic shared-memory limit of a kernel, set once per device (a process
+// may drive several GPUs; the attribute is per device context).
+template <class F>
+cudaError_t smem_attr_once(F* fn, int bytes, unsigned long long* done_mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (__atomic_load_n(done_mask, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) __atomic_fetch_or(done_mask, bit, __ATOMIC_RELEASE);
+    return e;
+}
+
 constexpr size_t kSmemBytes = sizeof(PairSmem) + 1024;
 static_assert(kSmemBytes <= 232448, "fa_pair shared memory exceeds 227 KB");
 
@@ -1458,13 +1482,8 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     P.kv_head_rows = static_cast<int>(f.kv_hs / kD);
     P.kv_row_rows = static_cast<int>(f.kv_rs / kD);
     P.T_n = static_cast<int>((n + kB - 1) / kB);
-    static bool attr_set[5] = {false, false, false, false, false};
-    if (!attr_set[MODE]) {
-        if ((e = cudaFuncSetAttribute(fa_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kSmemBytes))))
-            return e;
-        attr_set[MODE] = true;
-    }
+    static unsigned long long attr_done = 0;  // per MODE instantiation, bit per device
+    if ((e = smem_attr_once(fa_pair<MODE>, static_cast<int>(kSmemBytes), &attr_done))) return e;
     const int ipg = (P.step + 1) / 2;
     const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
     P.cluster = 1;
@@ -1505,19 +1524,21 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     return launch_cluster(P, grid, s);
 }
 
-cudaError_t convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s) {
+cudaError_t convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s,
+                      unsigned* overflow) {
     const int64_t total8 = f.hkv * f.geo.n * (kD / 8);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total8 + 255) / 256, 148 * 16));
     k_v_to_f16<<<blocks, 256, 0, s>>>(f.geo.n, f.hkv, f.kv_rs, f.kv_hs,
                                       static_cast<const __nv_bfloat16*>(v),
-                                      static_cast<__half*>(v16));
+                                      static_cast<__half*>(v16), overflow);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s) {
-    return convert_v(f, v, v16, s);
+cudaError_t fast_convert_v(const FastArgs& f, const void* v, void* v16, cudaStream_t s,
+                           unsigned* overflow) {
+    return convert_v(f, v, v16, s, overflow);
 }
 
 cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const void* v16, float* m,
@@ -1575,18 +1596,13 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     }
     constexpr size_t smem = sizeof(IdSmem) + 1024;
     static_assert(smem <= 232448, "k_identify_tc shared memory exceeds 227 KB");
-    static bool attr = false;
-    static int sms = 0;
-    if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_identify_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)))) {
-            if (own) cudaFreeAsync(split, s);
-            return e;
-        }
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        attr = true;
+    static unsigned long long attr_done = 0;
+    int sms = 0, dev = 0;
+    if ((e = smem_attr_once(k_identify_tc, static_cast<int>(smem), &attr_done)) ||
+        (e = cudaGetDevice(&dev)) ||
+        (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) {
+        if (own) cudaFreeAsync(split, s);
+        return e;
     }
     IdWork w;
     w.geo = f.geo;

@@ -51,6 +51,14 @@ cudaError_t launch_computed(const Geo& geo, int64_t hq, int64_t covered, const i
                             int64_t* computed, cudaStream_t s);
 // offsets[g] = stripe_offset(g) for g in [0, groups] (capacity layout).
 cudaError_t launch_offsets(const Geo& geo, int64_t* offsets, cudaStream_t s);
+// Stage-API list check / filter (see k_filter_lists): folded entries of each
+// caller list into out_idx at out_off (out_idx NULL = check only) and the
+// first out-of-range entry's (row << 32 | position) into *first_bad.
+cudaError_t launch_filter_lists(const Geo& geo, int64_t hq, const uint32_t* idx,
+                                const int32_t* counts, const int64_t* offsets, int64_t cap,
+                                bool csr, const int64_t* out_off, uint32_t* out_idx,
+                                int32_t* out_counts, unsigned long long* first_bad,
+                                cudaStream_t s);
 cudaError_t launch_add_u64(int64_t hq, int64_t covered, const unsigned long long* taken,
                            int64_t* computed, cudaStream_t s);
 

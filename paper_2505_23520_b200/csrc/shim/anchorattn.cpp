@@ -20,9 +20,11 @@ namespace anchorattn {
 
 namespace {
 
+// Default: the tcgen05 path wherever the shape allows it (the product); the
+// f64 exact path on request (ANCHORATTN_PRECISION=exact or set_precision).
 Precision g_precision = [] {
     const char* e = std::getenv("ANCHORATTN_PRECISION");
-    return (e && std::string(e) == "bf16") ? Precision::Bf16 : Precision::Exact;
+    return (e && std::string(e) == "exact") ? Precision::Exact : Precision::Bf16;
 }();
 
 void check(aa_status s) {
@@ -406,9 +408,9 @@ SparseResult sparse_attention(const HeadWorkload& w, const AnchorState& state,
 
     const bool fast = use_fast(w.d, cfg);
     // CSR of the lists in fold order (FoldPlan shuffle, sparse_exec.cpp:58-64).
-    // The fast path folds 128-key tiles and needs the covered-index skip
-    // (sparse_exec.cpp:79-82) applied up front; the exact path replays the
-    // reference's chunking on the raw lists.
+    // The ABI skips covered / non-causal entries itself (sparse_exec.cpp:79-82:
+    // per row inside the chunks on the exact path, by a device compaction of
+    // each list on the fast path).
     std::vector<std::uint32_t> flat;
     std::vector<int64_t> offsets(groups + 1, 0);
     std::vector<std::int32_t> counts(groups, 0);
@@ -418,10 +420,6 @@ SparseResult sparse_attention(const HeadWorkload& w, const AnchorState& state,
             SplitMix rng{plan.shuffle_seed + g};
             for (std::size_t i = order.size(); i > 1; --i)
                 std::swap(order[i - 1], order[rng.next() % i]);
-        }
-        if (fast) {
-            const std::size_t ws = window_start_token(g, cfg, w.n);
-            std::erase_if(order, [&](std::uint32_t j) { return j < cfg.b_kv || j >= ws; });
         }
         offsets[g] = static_cast<int64_t>(flat.size());
         counts[g] = static_cast<std::int32_t>(order.size());

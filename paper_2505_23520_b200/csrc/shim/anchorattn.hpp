@@ -8,11 +8,13 @@
 // GPU; there is no CPU fallback (std::runtime_error without a device).
 //
 // Precision: the reference takes f32 matrices and computes in f64.  The
-// default Precision::Exact runs the ABI's exact path (f64 GPU kernels, results
-// equal to the reference up to f64 round-off).  Precision::Bf16 (or
-// ANCHORATTN_PRECISION=bf16) rounds Q/K/V to bf16 and runs the tcgen05 path
-// when b_q == b_kv == 128 and d == 128 (the paper's kernels are FP16,
-// R/../PAPER.md Alg. 1 "REQUIRE FP16"); other shapes stay on the exact path.
+// default Precision::Bf16 rounds Q/K/V to bf16 and runs the tcgen05 path
+// whenever b_q == b_kv == 128 and d == 128 (the paper's configuration; its
+// kernels are FP16, R/../PAPER.md Alg. 1 "REQUIRE FP16"), with the
+// north-star tolerances (O max-abs <= 2e-2, relative L2 <= 1e-3; stripe sets
+// equal outside +-1e-3 of the threshold); other shapes run the exact path.
+// Precision::Exact (or ANCHORATTN_PRECISION=exact) always runs the exact
+// path (f64 GPU kernels, results equal to the reference up to f64 round-off).
 #pragma once
 
 #include <cstddef>

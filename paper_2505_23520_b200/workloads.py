@@ -122,3 +122,94 @@ def gen_random_workload(n, d=128, hq=1, hkv=1, seed=0, device="cpu", dtype=torch
     k = torch.randn(hkv, n, d, generator=g, device=device)
     v = torch.randn(hkv, n, d, generator=g, device=device)
     return q.to(dtype), k.to(dtype), v.to(dtype)
+
+
+def gen_layer(n: int, hq: int, hkv: int, seed: int, device="cpu", kv_heads=None, q_range=None,
+              dtype=torch.bfloat16):
+    """The benchmark layer: KV head ``kvh`` and its ``hq // hkv`` query heads
+    come from ``gen_sink_workload`` with seed ``seed + kvh``, so any subset of
+    KV heads (a shard, or the heads a parity test checks) is generated
+    identically to the whole layer.  ``kv_heads`` (default all) selects KV
+    heads; ``q_range = (q_begin, q_end)`` keeps only those global query heads.
+    Returns (q [hq', n, d], k [hkv', n, d], v [hkv', n, d])."""
+    if hq % hkv:
+        raise ValueError("hq must be a multiple of hkv")
+    rep = hq // hkv
+    kv_heads = range(hkv) if kv_heads is None else kv_heads
+    q_begin, q_end = q_range if q_range is not None else (0, hq)
+    qs, ks, vs = [], [], []
+    for kvh in kv_heads:
+        q, k, v = gen_sink_workload(SinkWorkloadSpec(n=n, hq=rep, hkv=1, seed=seed + kvh),
+                                    device=device, dtype=dtype)
+        lo, hi = max(q_begin - kvh * rep, 0), min(q_end - kvh * rep, rep)
+        if hi > lo:
+            qs.append(q[lo:hi])
+        ks.append(k)
+        vs.append(v)
+    return torch.cat(qs).contiguous(), torch.cat(ks), torch.cat(vs)
+
+
+def gen_planted_stripes(n: int, stripe_cols, mass_fraction: float = 0.5, seed: int = 0,
+                        d: int = 128, hq: int = 1, hkv: int = 1, vanish=None, device="cpu",
+                        dtype=torch.bfloat16):
+    """O(N*d) planted-stripe heads (the construction of gen_planted_stripes,
+    R/src/workloads.cpp:198-291):
+
+    * q = N(0, 0.015^2) noise + u_sink (+ u_gate outside the optional
+      ``vanish = (begin, end)`` row range);
+    * k = N(0, 0.015^2) noise; the sink column k_0 += (level + 2) sqrt(d) u_sink;
+      each planted column k_c += level sqrt(d) u (u_gate when gated, else
+      u_sink); every other column k_j -= 5 sqrt(d) u_sink;
+    * v ~ N(0, 1);
+
+    with level = log(max(2, odds * n / |cols|)) + 1, odds = m / (1 - m) (the
+    reference's first attempt, :223-226).  The reference then verifies the
+    planted mass on an O(N^2) dense probability map and retries with a
+    higher level; that check is infeasible at 128k, so this generator keeps
+    the first-attempt level and leaves the measurement to the GPU recall
+    pass.  GQA: query heads of a KV head share its directions.  Values are
+    rounded to ``dtype``."""
+    if n < 1 or d < 1:
+        raise ValueError("gen_planted_stripes: n, d must be >= 1")
+    cols = sorted(set(int(c) for c in stripe_cols))
+    if not cols:
+        raise ValueError("gen_planted_stripes: stripe_cols must be non-empty")
+    if cols[-1] >= n or cols[0] < 0:
+        raise ValueError("gen_planted_stripes: stripe column out of range")
+    if not (0.0 < mass_fraction < 1.0):
+        raise ValueError("gen_planted_stripes: mass_fraction must be in (0, 1)")
+    if vanish is not None and (d < 2 or vanish[0] >= vanish[1]):
+        raise ValueError("gen_planted_stripes: bad vanish range")
+    if hq % hkv:
+        raise ValueError("hq must be a multiple of hkv")
+    rep = hq // hkv
+    sqrt_d = math.sqrt(d)
+    odds = mass_fraction / (1.0 - mass_fraction)
+    level = math.log(max(2.0, odds * n / len(cols))) + 1.0
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    f32 = torch.float32
+    # two orthonormal directions per KV head (Gram-Schmidt)
+    a = torch.randn(hkv, 2, d, generator=g, device=device, dtype=f32)
+    u_sink = _unit_rows(a[:, 0:1])
+    u_gate = _unit_rows(a[:, 1:2] - (a[:, 1:2] * u_sink).sum(-1, keepdim=True) * u_sink)
+    gated = vanish is not None
+    q = 0.015 * torch.randn(hq, n, d, generator=g, device=device, dtype=f32)
+    k = 0.015 * torch.randn(hkv, n, d, generator=g, device=device, dtype=f32)
+    v = torch.randn(hkv, n, d, generator=g, device=device, dtype=f32)
+    us_q = u_sink.repeat_interleave(rep, dim=0)
+    q += us_q
+    if gated:
+        inside = torch.zeros(n, device=device, dtype=f32)
+        inside[vanish[0]:min(vanish[1], n)] = 1.0
+        q += (1.0 - inside)[None, :, None] * u_gate.repeat_interleave(rep, dim=0)
+    coef = torch.full((n,), -5.0 * sqrt_d, device=device, dtype=f32)
+    cols_t = torch.tensor([c for c in cols if c != 0], device=device, dtype=torch.int64)
+    coef[0] = (level + 2.0) * sqrt_d
+    if gated:
+        coef[cols_t] = 0.0
+        k[:, cols_t] += level * sqrt_d * u_gate
+    else:
+        coef[cols_t] = level * sqrt_d
+    k += coef[None, :, None] * u_sink
+    return q.to(dtype), k.to(dtype), v.to(dtype)

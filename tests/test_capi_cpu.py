@@ -90,3 +90,48 @@ def test_pybind_module_surface():
         aa.anchor_region(99, aa.BlockConfig(128, 128, 16), 256)
     mask = aa.anchor_mask(512, aa.BlockConfig(64, 32, 2))
     assert mask.total_selected() == aa.anchor_covered_count(512, aa.BlockConfig(64, 32, 2))
+
+
+def test_make_problem_checks_v_and_dtypes():
+    """The ABI reads v with k's strides and q's dtype: mismatches are refused
+    before any call (capi.make_problem)."""
+    q = torch.zeros(4, 256, 128, dtype=torch.bfloat16)
+    k = torch.zeros(2, 256, 128, dtype=torch.bfloat16)
+    cfg = capi.BlockConfig()
+    capi.make_problem(q, k, cfg, k.clone())
+    with pytest.raises(TypeError):
+        capi.make_problem(q, k, cfg, k.half())
+    with pytest.raises(TypeError):
+        capi.make_problem(q, k.float(), cfg)
+    with pytest.raises(ValueError):
+        capi.make_problem(q, k, cfg, torch.zeros(2, 255, 128, dtype=torch.bfloat16))
+    # same shape, different layout (a transposed view of a [n, hkv, d] buffer)
+    v = torch.zeros(256, 2, 128, dtype=torch.bfloat16).transpose(0, 1)
+    with pytest.raises(ValueError, match="strides"):
+        capi.make_problem(q, k, cfg, v)
+
+
+def test_oracle_sparse_lists_equals_capacity_layout(oracle):
+    """The oracle's arbitrary-list sparse_attention (the checker of the
+    unfiltered-list GPU test) equals its capacity-layout form bit for bit."""
+    import numpy as np
+
+    from oracle.oracle import Cfg
+    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
+
+    n, cfg = 3000, Cfg(128, 128, 4, 12.0)
+    q, k, v = (x[0].float().numpy() for x in gen_sink_workload(SinkWorkloadSpec(n=n, hq=1, hkv=1, seed=4)))
+    m, l, acc = oracle.compute_anchor(q, k, v, cfg)
+    idx, cnt = oracle.identify(q, k, oracle.pooled_anchor(m, cfg), cfg)
+    offs = oracle.stripe_offsets(n, cfg)
+    lists = [idx[offs[g]:offs[g] + cnt[g]] for g in range(len(cnt))]
+    a = oracle.sparse(q, k, v, cfg, m, l, acc, idx, cnt)
+    b = oracle.sparse_lists(q, k, v, cfg, m, l, acc, lists)
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+    # and it skips what the reference skips: covered / out-of-window entries
+    # change nothing, duplicates count twice
+    wide = [list(x) + [0, 5, n - 1] for x in lists]
+    c = oracle.sparse_lists(q, k, v, cfg, m, l, acc, wide)
+    assert np.array_equal(a[0], c[0]) and a[1] == c[1]
+    with pytest.raises(IndexError):
+        oracle.sparse_lists(q, k, v, cfg, m, l, acc, [list(x) + [n] for x in lists])
