@@ -56,7 +56,10 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-n", type=int, default=32768, help="reference sample length")
+    ap.add_argument("--cpu-samples", type=int, default=3,
+                    help="sparse_attention sample steps of the cpu_baseline reference timing")
+    ap.add_argument("--no-dense-libs", action="store_true",
+                    help="skip the cuDNN / flashinfer dense comparators")
     return ap.parse_args()
 
 
@@ -134,20 +137,40 @@ def workload_str(args):
             f"theta={args.theta}, b=128, step={args.step_blocks} ({config_ref(args)})")
 
 
+def geometry(n, step, b=128):
+    """Closed forms of the reference's blocking (R/src/detail/geometry.hpp:22-85,
+    SURVEY.md Appendix A) in plain Python — shared by both arms, so the
+    reference arm loads nothing of this repo's native code.  Returns dict(G,
+    rows [G], covered (per head), cand [G] (middle-region keys per group))."""
+    T = (n + b - 1) // b
+    G = (T + step - 1) // step
+    rows, cand = [], []
+    covered = 0
+    for g in range(G):
+        rb = g * step * b
+        re_ = min(rb + step * b, n)
+        wsb = 1 if rb < 2 * b else rb // b - 1
+        ws = min(wsb * b, n)
+        mid_end = max(ws, min(b, n))
+        rows.append(re_ - rb)
+        cand.append(max(0, mid_end - b))
+        # rows i in [rb, re_): covered = min(b, i + 1) + max(0, i + 1 - ws)
+        lo = rb
+        hi1 = min(re_, b)  # rows with i + 1 <= b
+        if hi1 > lo:
+            covered += (lo + 1 + hi1) * (hi1 - lo) // 2
+            lo = hi1
+        covered += b * (re_ - lo)
+        w0 = max(rb, ws)  # rows with i + 1 > ws
+        if re_ > w0:
+            covered += (w0 + 1 - ws + re_ - ws) * (re_ - w0) // 2
+    return {"G": G, "rows": rows, "covered": covered, "cand": cand}
+
+
 def layer_geometry(n, step):
-    """covered positions and stripe candidates per head (closed form)."""
-    from paper_2505_23520_b200 import capi
-
-    cfg = capi.BlockConfig(128, 128, step, 12.0)
-    c = cfg.c()
-    import ctypes as C
-
-    covered = capi.lib().aa_anchor_covered_count(n, C.byref(c))
-    G = capi.lib().aa_group_count(n, C.byref(c))
-    offs = capi.stripe_offsets(n, cfg)
-    rows = [min((g + 1) * step * 128, n) - g * step * 128 for g in range(G)]
-    cand = sum((offs[g + 1] - offs[g]) * rows[g] for g in range(G))
-    return covered, cand
+    """covered positions and stripe candidate positions per head."""
+    g = geometry(n, step)
+    return g["covered"], sum(c * r for c, r in zip(g["cand"], g["rows"]))
 
 
 def layer_tiles(q, k, v, args, cfg):
@@ -199,77 +222,273 @@ def k2_mma_flops(args, kv_heads):
     return kv_heads * tiles * 2 * 2.0 * 128 ** 3
 
 
-def reference_sample(n_sample, heads, theta, step, seed, threads=None):
-    """Run the reference (oracle/_ref) anchor_attention on `heads` heads of the
-    synthetic workload at n_sample through its own parallel_for.  Returns
-    (wall_s, computed per head, candidates per head, covered per head)."""
-    import numpy as np
-
-    from oracle.oracle import Cfg, Reference
-    from paper_2505_23520_b200.workloads import SinkWorkloadSpec, gen_sink_workload
-
-    ref = Reference()
-    q, k, v = gen_sink_workload(SinkWorkloadSpec(n=n_sample, hq=heads, hkv=heads, seed=seed))
-    qn, kn, vn = (x.float().numpy() for x in (q, k, v))
-    if threads:
-        os.environ["ANCHOR_ATTN_THREADS"] = str(threads)
-    t0 = time.perf_counter()
-    _, computed = ref.layer(qn, kn, vn, Cfg(128, 128, step, theta))
-    wall = time.perf_counter() - t0
-    covered, cand = layer_geometry(n_sample, step)
-    return wall, computed, cand, covered
+def sample_group(s, G):
+    """Stripe group the reference times at sample step s: consecutive steps
+    pair a heavy group with a light one (G-1-j, j), j striding over the
+    lower half, so any two consecutive steps span the work distribution."""
+    j = (s // 2) * 7 % max(1, G // 2)
+    return G - 1 - j if s % 2 == 0 else j
 
 
-def cpu_estimate(args, n_sample, heads, threads):
-    """Reference CPU ms/layer for the full workload, extrapolated by work:
-    rate = computed positions / s on the sample; the full layer's computed
-    positions use the sample's measured stripe-selection fraction."""
-    wall, computed, cand_s, cov_s = reference_sample(n_sample, heads, args.theta,
-                                                     args.step_blocks, args.seed, threads)
-    sel_frac = float((computed - cov_s).sum()) / (heads * cand_s) if cand_s else 0.0
-    rate = float(computed.sum()) / wall
-    cov_L, cand_L = layer_geometry(args.n, args.step_blocks)
-    layer_positions = args.hq * (cov_L + sel_frac * cand_L)
-    ms = layer_positions / rate * 1e3
-    sample = (f"reference anchor_attention (oracle/_ref) on {heads} synthetic heads at "
-              f"n={n_sample} via its parallel_for ({threads} threads): {wall:.2f} s, "
-              f"{rate:.3e} positions/s; extrapolated to the {args.hq}-head n={args.n} layer by "
-              f"computed positions (selection fraction {sel_frac:.4f})")
-    return ms, sample, wall
+class ReferenceTimer:
+    """The reference CPU implementation (oracle/_ref: the unmodified
+    reference sources compiled by oracle/Makefile) timed on THIS layer — the
+    same GQA inputs, n, theta and step — through its own public API and its
+    own parallel_for (one head per task, ANCHOR_ATTN_THREADS = host cores).
+
+    * compute_anchor + identify_stripes run on every head of the layer once,
+      timed as they are (no extrapolation): ``t12``.
+    * sparse_attention is the bulk of the reference's time (SURVEY §8(a):
+      21.3 of 55 s per head at sparsity 0.97, ~85% at 0.85).  A sample step
+      runs it on one round of heads (one head per thread) with each head's
+      StripeIndex cut to one group (sample_group), against the same round
+      with every list emptied (``t0``: the per-head state copy and finalize
+      the reference does regardless).  The per-position cost
+      (t_step - t0) / positions is pooled over the steps (ratio estimator)
+      and applied to the layer's own selected positions (the reference's
+      identify output), round by round: rounds = ceil(H / threads).
+    The layer estimate is t12 + rounds * (t0 + cost * mean selected positions
+    per head of a round)."""
+
+    def __init__(self, q, k, v, n, step, theta):
+        import numpy as np
+
+        from oracle.oracle import Cfg, Reference
+
+        self.np = np
+        self.ref = Reference()
+        self.threads = self.ref.max_threads()
+        self.H = q.shape[0]
+        self.geo = geometry(n, step)
+        self.layer = self.ref.open_layer(q, k, v, Cfg(128, 128, step, theta))
+        t = time.perf_counter()
+        self.layer.anchor_identify()
+        self.t12 = time.perf_counter() - t
+        G = self.geo["G"]
+        self.counts = self.layer.counts(G)  # f_c per (head, group)
+        self.rows = np.array(self.geo["rows"], np.int64)
+        self.sel = (self.counts * self.rows[None, :]).sum(1)  # selected positions per head
+        self.round = min(self.H, self.threads)
+        self.rounds = (self.H + self.round - 1) // self.round
+        self.t0 = []  # per round: the pass with every list emptied
+        for r in range(self.rounds):
+            t = time.perf_counter()
+            self.layer.sparse_groups(self._groups(-2, r))
+            self.t0.append(time.perf_counter() - t)
+        self.num = 0.0  # sum of (t_step - t0[round])
+        self.den = 0.0  # sum of the sampled positions of each pass's slowest head
+        self.steps = []
+
+    def _groups(self, g, r):
+        """Group g kept on the heads of round r; the other heads sit out."""
+        keep = self.np.full(self.H, -3, self.np.int64)
+        keep[r * self.round:(r + 1) * self.round] = g
+        return keep
+
+    def sample(self, s):
+        g = sample_group(s, self.geo["G"])
+        r = s % self.rounds
+        heads = self.np.arange(r * self.round, min((r + 1) * self.round, self.H))
+        t = time.perf_counter()
+        self.layer.sparse_groups(self._groups(g, r))
+        dt = time.perf_counter() - t
+        # the pass lasts as long as its slowest head (one head per thread)
+        pos = float(self.counts[heads, g].max() * self.rows[g])
+        self.steps.append((s, g, r, dt, pos))
+        return dt - self.t0[r], pos
+
+    def account(self, dt, pos):
+        self.num += dt
+        self.den += pos
+
+    def layer_seconds(self):
+        per_pos = self.num / self.den if self.den > 0 else 0.0
+        k3 = 0.0
+        for r in range(self.rounds):
+            heads = self.sel[r * self.round:(r + 1) * self.round]
+            k3 += self.t0[r] + per_pos * float(heads.mean())
+        return self.t12 + k3, per_pos
+
+    def describe(self, per_pos):
+        return (f"reference anchor_attention stages (oracle/_ref, its own parallel_for over "
+                f"{self.threads} threads) on this layer's {self.H} heads: compute_anchor + "
+                f"identify_stripes measured whole ({self.t12:.1f} s); sparse_attention sampled on "
+                f"{len(self.steps)} (round, group) steps of {self.round} heads x 1 group "
+                f"(groups {sorted(set(g for _, g, _, _, _ in self.steps))}), "
+                f"{per_pos * 1e9:.1f} ns per folded position per head-task, fixed cost "
+                f"{sum(self.t0):.2f} s over the rounds, scaled by the layer's own selected positions "
+                f"({float(self.sel.sum()):.4e}) over {self.rounds} round(s)")
+
+    def close(self):
+        self.layer.close()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_measurement(q, k, v, args, samples):
+    """(ms/layer, cpu_baseline dict) of the reference on this layer."""
+    rt = ReferenceTimer(q, k, v, args.n, args.step_blocks, args.theta)
+    try:
+        for s in range(samples):
+            rt.account(*rt.sample(s))
+        sec, per_pos = rt.layer_seconds()
+        desc = rt.describe(per_pos)
+        threads = rt.threads
+    finally:
+        rt.close()
+    return sec * 1e3, {"value": sec * 1e3, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "cpu_model": cpu_model(), "sample": desc}
+
+
+def layer_config(args):
+    """The `config` object both arms print (identical for the same run)."""
+    return {"workload": workload_str(args), "global_batch": 1, "seq_len": args.n,
+            "heads": f"{args.hq}Q/{args.hkv}KV",
+            "parallelism": "heads sharded over ranks" if int(os.environ.get("WORLD_SIZE", "1")) > 1
+                           else "one device",
+            "l2": f"inputs larger than L2 (q/k/v {(args.hq + 2 * args.hkv) * args.n * D * 2 / 1e9:.2f} "
+                  "GB per layer vs 126 MB L2), no flush"}
 
 
 # ------------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """--impl reference: the reference CPU implementation on this layer (the
+    same inputs as our arm, generated by workloads.gen_layer), rank 0 only.
+    One step = one sparse_attention sample of ReferenceTimer; warm-up steps
+    are run and discarded; the line's value is the layer estimate from the
+    K timed steps."""
+    import numpy as np
+    import torch
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
-    # per-head reference seconds ~ 0.8 s at 4k, x ~2.2 per doubling (SURVEY probe)
-    n_sample = 4096
-    for cand in (8192, 16384, 32768):
-        if 0.8 * (2.2 ** ((cand // 4096).bit_length() - 1)) <= per_step_budget:
-            n_sample = cand
-    heads = threads
-    vals = []
-    sample = ""
-    for i in range(args.warmup + args.steps):
-        ms, sample, _ = cpu_estimate(args, n_sample, heads, threads)
-        if i >= args.warmup:
-            vals.append(ms)
-    value = statistics.mean(vals)
+    from paper_2505_23520_b200.workloads import gen_layer
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"  # the bench's generator stream
+    q, k, v = gen_layer(args.n, args.hq, args.hkv, args.seed, device=dev)
+    qn, kn, vn = (x.float().cpu().numpy() for x in (q, k, v))
+    del q, k, v
+    t_start = time.perf_counter()
+    rt = ReferenceTimer(qn, kn, vn, args.n, args.step_blocks, args.theta)
+    del qn, kn, vn
+    try:
+        for s in range(args.warmup):
+            rt.sample(s)
+        for s in range(args.warmup, args.warmup + args.steps):
+            rt.account(*rt.sample(s))
+        sec, per_pos = rt.layer_seconds()
+        desc = rt.describe(per_pos)
+        threads = rt.threads
+    finally:
+        rt.close()
+    value = sec * 1e3
+    wall = time.perf_counter() - t_start
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_str(args), "global_batch": 1,
-                   "seq_len": args.n, "parallelism": "host threads over heads"},
+        "config": layer_config(args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_wall_s": wall,
+        "note": ("a step is a bounded sample (one sparse_attention group per head of a round); "
+                 "value is the whole-layer estimate, not the sample's wall time"),
     }
     print(json.dumps(line), flush=True)
+
+
+def dense_library_baselines(q, k, v, barrier, reduce, reps=2):
+    """Dense causal GQA attention of the same layer through library kernels
+    (the comparators of the north-star bar, semantics R/src/oracle.cpp:66-94):
+    torch SDPA on its cuDNN backend and flashinfer's single-prefill kernels
+    (cutlass = the sm100 FMHA, fa2), each timed with CUDA events after one
+    warm-up call; an entry holds the error when a backend is unavailable."""
+    import torch
+    import torch.nn.functional as F
+
+    hq, n, d = q.shape
+    hkv = k.shape[0]
+    res = {}
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return reduce([a.elapsed_time(b) / reps], "max")[0]
+
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        q4, k4, v4 = q[None], k[None], v[None]
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            try:
+                res["torch_sdpa_cudnn"] = timed(
+                    lambda: F.scaled_dot_product_attention(q4, k4, v4, is_causal=True,
+                                                           enable_gqa=True))
+            except Exception:  # noqa: BLE001 - cuDNN without native GQA: K/V expanded
+                rep = hq // hkv
+                ke, ve = (x.repeat_interleave(rep, dim=1) for x in (k4, v4))
+                res["torch_sdpa_cudnn"] = timed(
+                    lambda: F.scaled_dot_product_attention(q4, ke, ve, is_causal=True))
+                res["torch_sdpa_cudnn_note"] = "K/V expanded to the query heads (no GQA entry)"
+                del ke, ve
+    except Exception as exc:  # noqa: BLE001 - reported in the line
+        res["torch_sdpa_cudnn"] = f"unavailable: {str(exc).splitlines()[0][:160]}"
+    torch.cuda.empty_cache()
+    try:
+        import flashinfer
+
+        qn = q.transpose(0, 1).contiguous()  # NHD
+        kn = k.transpose(0, 1).contiguous()
+        vn = v.transpose(0, 1).contiguous()
+        # the ragged-batch prefill wrapper carries flashinfer's Blackwell
+        # kernels: "cutlass" (the sm100 CUTLASS FMHA) and "cute-dsl" (the
+        # CuTe-DSL sm100 attention kernel); fa2 through the single-prefill entry
+        ind = torch.tensor([0, n], dtype=torch.int32, device=q.device)
+        for backend in ("cutlass", "cute-dsl"):
+            try:
+                ws = torch.empty(256 << 20, dtype=torch.uint8, device=q.device)
+                w = flashinfer.BatchPrefillWithRaggedKVCacheWrapper(ws, kv_layout="NHD",
+                                                                    backend=backend)
+                w.plan(ind, ind, hq, hkv, d, causal=True, q_data_type=q.dtype,
+                       kv_data_type=k.dtype)
+                res[f"flashinfer_{backend}"] = timed(lambda: w.run(qn, kn, vn))
+                del w, ws
+            except Exception as exc:  # noqa: BLE001
+                res[f"flashinfer_{backend}"] = f"unavailable: {str(exc).splitlines()[0][:160]}"
+        try:
+            res["flashinfer_fa2"] = timed(
+                lambda: flashinfer.single_prefill_with_kv_cache(qn, kn, vn, causal=True,
+                                                                backend="fa2"))
+        except Exception as exc:  # noqa: BLE001
+            res["flashinfer_fa2"] = f"unavailable: {str(exc).splitlines()[0][:160]}"
+        del qn, kn, vn
+    except Exception as exc:  # noqa: BLE001
+        res["flashinfer"] = f"unavailable: {str(exc).splitlines()[0][:160]}"
+    return res
+
+
+def best_dense(ours, libs):
+    vals = [x for x in [ours] + list((libs or {}).values()) if isinstance(x, (int, float))]
+    return min(vals) if vals else None
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -490,6 +709,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         dense_ms = reduce([a.elapsed_time(b) / reps], "max")[0]
         del dout
+    dense_libs = None
+    if not args.no_dense and not args.no_dense_libs:
+        dense_libs = dense_library_baselines(q, k, v, barrier, reduce)
+        torch.cuda.empty_cache()
 
     # e2e through the host-buffer C ABI entry (pinned host tensors)
     e2e = None
@@ -543,10 +766,14 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            threads = os.cpu_count() or 1
-            ms_cpu, sample, _ = cpu_estimate(args, args.cpu_n, threads, threads)
-            cpu = {"value": ms_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": sample}
+            del pipe
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        try:
+            qn, kn, vn = (x.float().cpu().numpy() for x in (q, k, v))
+            _, cpu = reference_measurement(qn, kn, vn, args, args.cpu_samples)
+            del qn, kn, vn
         except Exception as exc:  # noqa: BLE001 - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -556,18 +783,18 @@ def run_ours(args):
             "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_str(args),
-                       "global_batch": 1, "seq_len": args.n,
-                       "parallelism": (f"kv-head shard x{world}" if world <= args.hkv else
-                                       f"query-head runs of each KV head x{world}") if world > 1
-                                      else "single GPU",
-                       "l2": f"inputs larger than L2 (q/k/v {(args.hq + 2 * args.hkv) * args.n * D * 2 / 1e9:.2f} "
-                             "GB per layer vs 126 MB L2), no flush"},
+            "config": layer_config(args),
+            "placement": (f"kv-head shard x{world}" if world <= args.hkv else
+                          f"query-head runs of each KV head x{world}") if world > 1 else "single GPU",
             "sparsity": sparsity, "recall": recall, "computed_positions": comp_total,
             "stage_ms": dict(zip(capi.STAGES, stage_ms)),
             "kernels": kernels,
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms) if dense_ms else None,
+            "dense_library_ms": dense_libs,
+            "dense_best_ms": best_dense(dense_ms, dense_libs),
+            "speedup_vs_best_dense": (best_dense(dense_ms, dense_libs) / ms)
+                                     if best_dense(dense_ms, dense_libs) else None,
             "graph": graph,
             "roofline": roofline,
             "cpu_baseline": cpu,

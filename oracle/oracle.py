@@ -298,6 +298,16 @@ class Reference:
         L.ref_gen_sink_local.restype = C.c_int
         L.ref_gen_sink_local.argtypes = [_i64, _i64, _f64, _i64, C.c_uint64, _p, _p, _p]
         L.ref_max_threads.restype = _i64
+        L.ref_layer_open.restype = _p
+        L.ref_layer_open.argtypes = [_i64, _i64, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _f64]
+        L.ref_layer_close.restype = None
+        L.ref_layer_close.argtypes = [_p]
+        L.ref_layer_anchor_identify.restype = C.c_int
+        L.ref_layer_anchor_identify.argtypes = [_p, C.c_int]
+        L.ref_layer_counts.restype = C.c_int
+        L.ref_layer_counts.argtypes = [_p, _p]
+        L.ref_layer_sparse_groups.restype = C.c_int
+        L.ref_layer_sparse_groups.argtypes = [_p, _p, _p]
 
     def _check(self, rc):
         if rc != 0:
@@ -361,3 +371,47 @@ class Reference:
 
     def max_threads(self) -> int:
         return int(self.L.ref_max_threads())
+
+    def open_layer(self, q, k, v, cfg: Cfg) -> "RefLayer":
+        return RefLayer(self, q, k, v, cfg)
+
+
+class RefLayer:
+    """A GQA layer (q [H, n, d], k/v [Hkv, n, d]) resident in the reference's
+    own types, for stage-by-stage timing (oracle/ref_driver.cpp ref_layer_*)."""
+
+    def __init__(self, ref: Reference, q, k, v, cfg: Cfg):
+        self.ref = ref
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        self.H, self.n, self.d = q.shape
+        self.cfg = cfg
+        self.h = ref.L.ref_layer_open(self.H, k.shape[0], self.n, self.d, _ptr(q), _ptr(k), _ptr(v),
+                                      cfg.b_q, cfg.b_kv, cfg.step, float(cfg.theta))
+        if not self.h:
+            raise RuntimeError(ref.L.ref_last_error().decode())
+
+    def close(self):
+        if self.h:
+            self.ref.L.ref_layer_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def anchor_identify(self, zero_anchor=False):
+        """compute_anchor + identify_stripes on every head (parallel_for)."""
+        self.ref._check(self.ref.L.ref_layer_anchor_identify(self.h, int(zero_anchor)))
+
+    def counts(self, groups: int) -> np.ndarray:
+        c = np.zeros((self.H, groups), np.int64)
+        self.ref.L.ref_layer_counts(self.h, _ptr(c))
+        return c
+
+    def sparse_groups(self, group_of_head) -> np.ndarray:
+        """sparse_attention per head keeping only group group_of_head[h] of its
+        StripeIndex (-1: all groups, -2: none, -3: head left out of the pass).
+        Returns computed positions."""
+        g = np.ascontiguousarray(group_of_head, np.int64)
+        out = np.zeros(self.H, np.int64)
+        self.ref._check(self.ref.L.ref_layer_sparse_groups(self.h, _ptr(g), _ptr(out)))
+        return out

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "anchorattn/anchor_pass.hpp"
 #include "anchorattn/metrics.hpp"
@@ -186,6 +187,98 @@ int ref_gen_sink_local(std::int64_t n, std::int64_t d, double sink_strength,
         std::memcpy(q, w.q.data.data(), static_cast<std::size_t>(n * d) * 4);
         std::memcpy(k, w.k.data.data(), static_cast<std::size_t>(n * d) * 4);
         std::memcpy(v, w.v.data.data(), static_cast<std::size_t>(n * d) * 4);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// A layer held across calls, for stage-sampled timing of the reference in
+// bench.py (reference arm and cpu_baseline).  Every stage runs the reference's
+// own public functions over its own parallel_for (one head per task):
+//   ref_layer_anchor_identify  compute_anchor + identify_stripes, all heads
+//   ref_layer_sparse_groups    sparse_attention, each head's StripeIndex cut
+//                              down to one group (the rest emptied; the
+//                              reference then only copies / finalizes their
+//                              rows), or the whole index (group -1), or
+//                              nothing (group -2: the fixed per-head cost);
+//                              group -3 leaves the head out of the pass
+struct RefLayer {
+    BlockConfig cfg;
+    std::vector<HeadWorkload> w;
+    std::vector<AnchorState> st;
+    std::vector<StripeIndex> si;
+};
+
+void* ref_layer_open(std::int64_t heads, std::int64_t kv_heads, std::int64_t n, std::int64_t d,
+                     const float* q, const float* k, const float* v, std::int64_t b_q,
+                     std::int64_t b_kv, std::int64_t step, double theta) {
+    try {
+        auto* L = new RefLayer;
+        L->cfg = cfg_of(b_q, b_kv, step, theta);
+        const std::int64_t per = heads / kv_heads;
+        const std::size_t hd = static_cast<std::size_t>(n * d);
+        L->w.resize(static_cast<std::size_t>(heads));
+        L->st.resize(static_cast<std::size_t>(heads));
+        L->si.resize(static_cast<std::size_t>(heads));
+        parallel_for(static_cast<std::size_t>(heads), [&](std::size_t h) {
+            const std::size_t kvh = h / static_cast<std::size_t>(per);
+            L->w[h] = HeadWorkload::create(mat(q + h * hd, n, d), mat(k + kvh * hd, n, d),
+                                           mat(v + kvh * hd, n, d));
+        });
+        return L;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_layer_close(void* handle) { delete static_cast<RefLayer*>(handle); }
+
+int ref_layer_anchor_identify(void* handle, int zero_anchor) {
+    try {
+        auto* L = static_cast<RefLayer*>(handle);
+        parallel_for(L->w.size(), [&](std::size_t h) {
+            L->st[h] = compute_anchor(L->w[h], L->cfg);
+            L->si[h] = zero_anchor ? identify_stripes_zero_anchor(L->w[h], L->cfg)
+                                   : identify_stripes(L->w[h], L->st[h], L->cfg);
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// f_c per (head, group): counts [heads * groups].
+int ref_layer_counts(void* handle, std::int64_t* counts) {
+    auto* L = static_cast<RefLayer*>(handle);
+    std::size_t o = 0;
+    for (const StripeIndex& s : L->si)
+        for (const auto& g : s.groups) counts[o++] = static_cast<std::int64_t>(g.size());
+    return 0;
+}
+
+int ref_layer_sparse_groups(void* handle, const std::int64_t* group_of_head,
+                            std::int64_t* computed) {
+    try {
+        auto* L = static_cast<RefLayer*>(handle);
+        parallel_for(L->w.size(), [&](std::size_t h) {
+            const std::int64_t keep = group_of_head[h];
+            if (keep == -3) {  // head not in this pass
+                computed[h] = 0;
+                return;
+            }
+            StripeIndex sub = L->si[h];
+            if (keep != -1)
+                for (std::size_t g = 0; g < sub.groups.size(); ++g)
+                    if (static_cast<std::int64_t>(g) != keep) sub.groups[g].clear();
+            const SparseResult res = sparse_attention(L->w[h], L->st[h], sub, L->cfg);
+            computed[h] = static_cast<std::int64_t>(res.stats.computed_positions);
+        });
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -142,7 +142,7 @@ def test_sparse_out_of_range_index(dtype):
     with pytest.raises(IndexError, match=f"sparse_attention: stripe index {n + 5} out of range"):
         capi.sparse(q, k, v, st, bad, counts, cfg)
     # a later bad entry does not mask the first one
-    bad[h, offs[g] + 3] = 2 ** 31 + 7
+    bad[h, offs[g] + 3] = -5  # 4294967291 as uint32
     with pytest.raises(IndexError, match=f"stripe index {n + 5} out of range"):
         capi.sparse(q, k, v, st, bad, counts, cfg)
 

@@ -95,3 +95,23 @@ def test_sharded_layer_equals_full_layer():
         torch.cuda.synchronize()
         assert torch.equal(torch.cat(parts), full)
         assert torch.equal(torch.cat(comps), comp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,hq,hkv", [(2, 32, 8), (8, 28, 4)])
+def test_torchrun_sharded_chain(world, hq, hkv):
+    """torchrun, one process per rank (all on the test box's one GPU, gloo
+    for the gather): each rank runs the real chain on its shard — KV-head
+    blocks (Llama 32/8 over 2) or query-head runs of unequal length (Qwen 28/4
+    over 8: 3 + 4 query heads per KV head) — and the gathered output and
+    computed counts equal the single-rank layer bit for bit."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "tests", "shard_worker.py"), "16384", str(hq), str(hkv)]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert f"SHARD_CHECK world={world} {hq}/{hkv} n=16384: OK" in r.stdout
