@@ -491,6 +491,72 @@ def best_dense(ours, libs):
     return min(vals) if vals else None
 
 
+def run_units_timing(args, units, q, k, v, q0, kv0, dev, world, rank, reduce, gather_all):
+    """A rank whose share holds split heads (query-group ranges): every step
+    runs its WorkUnits through the C ABI (aa_anchor_attention_groups); the
+    line reports ms/layer (max over ranks), the per-rank times and the
+    imbalance.  Per-kernel metrics need a whole-head shard and are omitted."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_23520_b200 import capi
+
+    cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
+    calls = []
+    for u in units:
+        qs = q[u.q_begin - q0:u.q_end - q0]
+        ks, vs = k[u.kv_begin - kv0:u.kv_end - kv0], v[u.kv_begin - kv0:u.kv_end - kv0]
+        calls.append((u, qs, ks, vs, capi.Pipeline(qs, ks, vs, cfg),
+                      torch.empty((qs.shape[0], args.n, D), dtype=torch.float32, device=dev),
+                      torch.empty(qs.shape[0], dtype=torch.int64, device=dev)))
+
+    def step():
+        for u, qs, ks, vs, pipe, out, comp in calls:
+            pipe(qs, ks, vs, out=out, computed=comp, groups=(u.g_begin, u.g_end))
+
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_local = t0.elapsed_time(t1) / args.steps
+    rank_ms = gather_all(ms_local)
+    ms = max(rank_ms)
+    comp_total = int(reduce([float(sum(int(c.sum()) for *_, c in calls))], "sum")[0])
+    print(f"[bench] rank {rank}: {ms_local:.3f} ms/layer-shard over {len(units)} units", file=sys.stderr,
+          flush=True)
+    if rank == 0:
+        causal = args.n * (args.n + 1) // 2
+        line = {
+            "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": layer_config(args),
+            "placement": f"balanced (query head, query group) units x{world} (sharding.shard_work)",
+            "rank_ms": rank_ms, "imbalance": max(rank_ms) / (sum(rank_ms) / len(rank_ms)),
+            "sparsity": 1.0 - comp_total / (args.hq * causal), "computed_positions": comp_total,
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "note": "a rank holds split heads: per-kernel metrics, e2e and the CPU baseline are "
+                    "reported by whole-head shards (the default configurations)",
+            "gpu_launches": sum(9 for _ in units) * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -524,21 +590,32 @@ def run_ours(args):
                             group=host_group)
         return t.tolist()
 
-    from paper_2505_23520_b200.sharding import shard_heads
+    from paper_2505_23520_b200.sharding import shard_work
 
-    try:
-        shard = shard_heads(args.hq, args.hkv, rank, world)
-    except ValueError as exc:
-        raise SystemExit(f"cannot shard {args.hq}/{args.hkv} heads over {world} ranks: {exc}")
-    rep = args.hq // args.hkv
-    kv_local = shard.kv_heads
+    def gather_all(x):
+        """one host float from every rank (rank order)"""
+        if world == 1:
+            return [x]
+        t = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(t, torch.tensor([x], dtype=torch.float64), group=host_group)
+        return [float(v[0]) for v in t]
 
-    # this rank's KV heads and their query heads (KV-head blocks, or with more
-    # ranks than KV heads a run of one KV head's query heads); each KV head is
-    # generated from its own seed so the data does not depend on the rank count
+    # this rank's balanced share of the layer's (query head, query group)
+    # units (sharding.shard_work): whole KV heads when they split evenly
+    # (Llama 32/8 over 1/2/4/8 ranks), else query heads split by query-group
+    # ranges; each KV head is generated from its own seed so the data does not
+    # depend on the rank count
+    G_all = geometry(args.n, args.step_blocks)["G"]
+    units = shard_work(args.hq, args.hkv, rank, world, args.n, args.step_blocks)
+    kv0, kv1 = min(u.kv_begin for u in units), max(u.kv_end for u in units)
+    q0, q1 = min(u.q_begin for u in units), max(u.q_end for u in units)
     q, k, v = gen_layer(args.n, args.hq, args.hkv, args.seed, device=dev,
-                        kv_heads=range(shard.kv_begin, shard.kv_end),
-                        q_range=(shard.q_begin, shard.q_end))
+                        kv_heads=range(kv0, kv1), q_range=(q0, q1))
+    if not (len(units) == 1 and (units[0].g_begin, units[0].g_end) == (0, G_all)):
+        return run_units_timing(args, units, q, k, v, q0, kv0, dev, world, rank, reduce,
+                                gather_all)
+    rep = args.hq // args.hkv
+    kv_local = kv1 - kv0
     cfg = capi.BlockConfig(128, 128, args.step_blocks, args.theta)
     pipe = capi.Pipeline(q, k, v, cfg)
     hq_local = q.shape[0]
@@ -585,6 +662,7 @@ def run_ours(args):
     comp_local = int(computed.sum().item())
     covered, cand = layer_geometry(args.n, args.step_blocks)
     ms = reduce([ms_local], "max")[0]
+    rank_ms = gather_all(ms_local)
     comp_total = int(reduce([comp_local], "sum")[0])
     causal = args.n * (args.n + 1) // 2
     sparsity = 1.0 - comp_total / (args.hq * causal)
@@ -784,8 +862,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": layer_config(args),
-            "placement": (f"kv-head shard x{world}" if world <= args.hkv else
-                          f"query-head runs of each KV head x{world}") if world > 1 else "single GPU",
+            "placement": f"whole KV heads per rank x{world} (sharding.shard_work)" if world > 1
+                         else "single GPU",
+            "rank_ms": rank_ms,
+            "imbalance": max(rank_ms) / (sum(rank_ms) / len(rank_ms)),
             "sparsity": sparsity, "recall": recall, "computed_positions": comp_total,
             "stage_ms": dict(zip(capi.STAGES, stage_ms)),
             "kernels": kernels,

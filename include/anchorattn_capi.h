@@ -166,6 +166,19 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
                               int zero_anchor, void* out, aa_dtype out_dtype, int64_t* computed,
                               void* workspace, size_t workspace_bytes, aa_stream_t stream);
 
+/* The same chain for the query groups [group_begin, group_end) of every head
+ * only (groups of step * b_q rows, R/src/detail/geometry.hpp:36-47): reads
+ * their q rows and K/V rows [0, row_end(group_end - 1)), writes their rows of
+ * out, and computed[h] = the positions those rows compute.  Groups are
+ * independent given the K/V prefix (R/../SPEC.md), so a layer split into
+ * group ranges — e.g. balanced multi-GPU shards of a head
+ * (paper_2505_23520_b200.sharding.shard_work) — reproduces the whole-layer
+ * result bit for bit.  bf16 (tcgen05) path only. */
+aa_status aa_anchor_attention_groups(const aa_problem* p, int64_t group_begin, int64_t group_end,
+                                     const void* q, const void* k, const void* v, int zero_anchor,
+                                     void* out, aa_dtype out_dtype, int64_t* computed,
+                                     void* workspace, size_t workspace_bytes, aa_stream_t stream);
+
 /* Same chain on HOST buffers (the reference's value-semantics calling
  * convention, bindings.cpp:21-32): copies q/k/v in, runs, copies out and the
  * per-head computed counts back; blocks until done.  Device buffers, streams

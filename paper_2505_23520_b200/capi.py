@@ -77,6 +77,8 @@ def lib():
             "aa_sparse_attention": [P, p, p, p, p, p, p, p, p, p, C.c_int64, p, C.c_int, p, p],
             "aa_finalize_anchor": [P, p, p, p, C.c_int, p],
             "aa_anchor_attention": [P, p, p, p, C.c_int, p, C.c_int, p, p, C.c_size_t, p],
+            "aa_anchor_attention_groups": [P, C.c_int64, C.c_int64, p, p, p, C.c_int, p, C.c_int, p, p,
+                                           C.c_size_t, p],
             "aa_anchor_attention_host": [P, p, p, p, C.c_int, p, C.c_int, p],
             "aa_dense_attention": [P, p, p, p, p, C.c_int, p],
             "aa_union_recall": [P, p, p, p, p, p, p],
@@ -207,7 +209,10 @@ class Pipeline:
         self.workspace = torch.empty(self.plan.workspace_bytes, dtype=torch.uint8, device=q.device)
 
     def __call__(self, q, k, v, zero_anchor=False, out=None, out_dtype=torch.float32,
-                 computed=None):
+                 computed=None, groups=None):
+        """The chain (aa_anchor_attention); ``groups=(g0, g1)`` runs only the
+        query groups [g0, g1) of every head (aa_anchor_attention_groups: the
+        other rows of ``out`` are left untouched)."""
         _same_layout(self.p, q, k, v)
         hq, n, d = q.shape
         if out is None:
@@ -216,10 +221,17 @@ class Pipeline:
             raise ValueError("out must be a contiguous [hq, n, d] tensor on q's device")
         if computed is None:
             computed = torch.empty(hq, dtype=torch.int64, device=q.device)
-        _check(lib().aa_anchor_attention(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v),
-                                         int(zero_anchor), _ptr(out), _out_code(out.dtype),
-                                         _ptr(computed), _ptr(self.workspace),
-                                         self.plan.workspace_bytes, _stream()))
+        if groups is None:
+            _check(lib().aa_anchor_attention(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v),
+                                             int(zero_anchor), _ptr(out), _out_code(out.dtype),
+                                             _ptr(computed), _ptr(self.workspace),
+                                             self.plan.workspace_bytes, _stream()))
+        else:
+            _check(lib().aa_anchor_attention_groups(C.byref(self.p), int(groups[0]), int(groups[1]),
+                                                    _ptr(q), _ptr(k), _ptr(v), int(zero_anchor),
+                                                    _ptr(out), _out_code(out.dtype), _ptr(computed),
+                                                    _ptr(self.workspace),
+                                                    self.plan.workspace_bytes, _stream()))
         return out, computed
 
 

@@ -136,7 +136,16 @@ aa::FastArgs fast_args(const aa_problem& p) {
     f.kv_rs = p.kv_row_stride ? p.kv_row_stride : p.d;
     f.kv_hs = p.kv_head_stride ? p.kv_head_stride : p.n * f.kv_rs;
     f.theta = p.cfg.theta;
+    f.g0 = 0;
+    f.g1 = f.geo.groups();
     return f;
+}
+
+// Anchor-covered positions of the rows of groups [g0, g1) (per head).
+int64_t covered_in_groups(const aa::Geo& G, int64_t g0, int64_t g1) {
+    int64_t total = 0;
+    for (int64_t i = G.row_begin(g0); i < G.row_end(g1 - 1); ++i) total += G.covered_count_for_row(i);
+    return total;
 }
 
 // Stream-ordered temporary (cudaMallocAsync pool) freed on scope exit.
@@ -343,20 +352,24 @@ static aa_status identify_impl(const aa_problem* p, const aa_plan& plan, const v
                                const float* qbar, const double* anchor, int zero_anchor,
                                uint32_t* indices, int32_t* counts, int64_t* offsets_dev,
                                uint32_t* bits, int64_t words_per_row, cudaStream_t st,
-                               void* scratch = nullptr, size_t scratch_bytes = 0) {
+                               void* scratch = nullptr, size_t scratch_bytes = 0,
+                               int64_t g0 = 0, int64_t g1 = -1) {
     const aa::Geo G = geo_of(p->n, p->cfg);
+    if (g1 < 0) g1 = G.groups();
     const double* ref = zero_anchor ? nullptr : anchor;
     if (p->dtype == AA_F32) {
         AA_CUDA(aa::launch_identify_exact(exact_args(*p), static_cast<const float*>(k), qbar, ref,
                                           bits, words_per_row, st));
     } else {
-        AA_CUDA(aa::fast_identify(fast_args(*p), k, qbar, ref, bits, words_per_row, st, scratch,
-                                  scratch_bytes));
+        aa::FastArgs f = fast_args(*p);
+        f.g0 = g0;
+        f.g1 = g1;
+        AA_CUDA(aa::fast_identify(f, k, qbar, ref, bits, words_per_row, st, scratch, scratch_bytes));
     }
     AA_CUDA(aa::launch_offsets(G, offsets_dev, st));
     AA_CUDA(aa::launch_compact(G, p->hq, bits, words_per_row, offsets_dev,
                                plan.stripe_capacity > 0 ? plan.stripe_capacity : 1, indices,
-                               counts, st));
+                               counts, st, g0, g1));
     return AA_OK;
 }
 
@@ -497,6 +510,52 @@ aa_status aa_finalize_anchor(const aa_problem* p, const void* l, const void* acc
     return AA_OK;
 }
 
+// The fast path's fused chain (V->f16, K1, pool, K2 + compaction, K3,
+// stats) over the query groups [g0, g1) of every head.
+static aa_status fused_fast(const aa_problem* p, const aa_plan& plan, const Layout& L,
+                            const void* q, const void* k, const void* v, int zero_anchor,
+                            void* out, aa_dtype out_dtype, int64_t* computed, cudaStream_t st,
+                            int64_t g0, int64_t g1) {
+    const aa::Geo G = geo_of(p->n, p->cfg);
+    const int64_t cap = plan.stripe_capacity > 0 ? plan.stripe_capacity : 1;
+    aa::FastArgs f = fast_args(*p);
+    f.g0 = g0;
+    f.g1 = g1;
+    mark(0, st);
+    AA_CUDA(cudaMemsetAsync(L.flags, 0, 8, st));
+    AA_CUDA(aa::fast_convert_v(f, v, L.v16, st, static_cast<unsigned*>(L.flags)));
+    mark(1, st);
+    AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
+                            static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
+                            static_cast<double*>(L.msum), st, /*acc_f16=*/true));
+    mark(2, st);
+    AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
+                          static_cast<double*>(L.msum), static_cast<double*>(L.anchor),
+                          static_cast<float*>(L.qbar), st));
+    if (aa_status s = identify_impl(p, plan, k, static_cast<float*>(L.qbar),
+                                    static_cast<double*>(L.anchor), zero_anchor,
+                                    static_cast<uint32_t*>(L.indices),
+                                    static_cast<int32_t*>(L.counts),
+                                    static_cast<int64_t*>(L.offsets),
+                                    static_cast<uint32_t*>(L.bits), L.words_per_row, st, L.split,
+                                    L.split_bytes, g0, g1))
+        return s;
+    mark(3, st);
+    AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
+                            static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
+                            static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
+                            false, out, out_dtype, st, /*acc_f16=*/true));
+    mark(4, st);
+    if (computed) {
+        const int64_t covered = (g0 == 0 && g1 == plan.groups) ? plan.covered_positions
+                                                               : covered_in_groups(G, g0, g1);
+        AA_CUDA(aa::launch_computed(G, p->hq, covered, static_cast<int32_t*>(L.counts), computed, st,
+                                    g0, g1));
+    }
+    mark(5, st);
+    return AA_OK;
+}
+
 aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k, const void* v,
                               int zero_anchor, void* out, aa_dtype out_dtype, int64_t* computed,
                               void* workspace, size_t workspace_bytes, aa_stream_t stream) {
@@ -545,37 +604,34 @@ aa_status aa_anchor_attention(const aa_problem* p, const void* q, const void* k,
                                        static_cast<unsigned long long*>(L.taken), computed, st));
         return AA_OK;
     }
-    const aa::FastArgs f = fast_args(*p);
-    mark(0, st);
-    AA_CUDA(cudaMemsetAsync(L.flags, 0, 8, st));
-    AA_CUDA(aa::fast_convert_v(f, v, L.v16, st, static_cast<unsigned*>(L.flags)));
-    mark(1, st);
-    AA_CUDA(aa::fast_anchor(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
-                            static_cast<float*>(L.acc), static_cast<float*>(L.qsum),
-                            static_cast<double*>(L.msum), st, /*acc_f16=*/true));
-    mark(2, st);
-    AA_CUDA(aa::fast_pool(f, q, static_cast<float*>(L.m), static_cast<float*>(L.qsum),
-                          static_cast<double*>(L.msum), static_cast<double*>(L.anchor),
-                          static_cast<float*>(L.qbar), st));
-    if (aa_status s = identify_impl(p, plan, k, static_cast<float*>(L.qbar),
-                                    static_cast<double*>(L.anchor), zero_anchor,
-                                    static_cast<uint32_t*>(L.indices),
-                                    static_cast<int32_t*>(L.counts),
-                                    static_cast<int64_t*>(L.offsets),
-                                    static_cast<uint32_t*>(L.bits), L.words_per_row, st, L.split,
-                                    L.split_bytes))
-        return s;
-    mark(3, st);
-    AA_CUDA(aa::fast_sparse(f, q, k, L.v16, static_cast<float*>(L.m), static_cast<float*>(L.l),
-                            static_cast<float*>(L.acc), static_cast<uint32_t*>(L.indices),
-                            static_cast<int32_t*>(L.counts), static_cast<int64_t*>(L.offsets), cap,
-                            false, out, out_dtype, st, /*acc_f16=*/true));
-    mark(4, st);
-    if (computed)
-        AA_CUDA(aa::launch_computed(G, p->hq, plan.covered_positions,
-                                    static_cast<int32_t*>(L.counts), computed, st));
-    mark(5, st);
-    return AA_OK;
+    return fused_fast(p, plan, L, q, k, v, zero_anchor, out, out_dtype, computed, st, 0,
+                      plan.groups);
+}
+
+aa_status aa_anchor_attention_groups(const aa_problem* p, int64_t group_begin, int64_t group_end,
+                                     const void* q, const void* k, const void* v, int zero_anchor,
+                                     void* out, aa_dtype out_dtype, int64_t* computed,
+                                     void* workspace, size_t workspace_bytes, aa_stream_t stream) {
+    aa_plan plan;
+    if (aa_status s = aa_make_plan(p, &plan)) return s;
+    if (p->dtype != AA_BF16)
+        return fail(AA_ERR_UNSUPPORTED, "aa_anchor_attention_groups: bf16 (tcgen05) path only");
+    if (group_begin < 0 || group_end > plan.groups || group_begin >= group_end)
+        return fail(AA_ERR_INVALID_ARGUMENT, "aa_anchor_attention_groups: empty or out-of-range group range");
+    if (out_dtype != AA_F32 && out_dtype != AA_BF16)
+        return fail(AA_ERR_INVALID_ARGUMENT, "out_dtype must be AA_F32 or AA_BF16");
+    if (aa_status s = require_device()) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Temp tmp(st);
+    if (!workspace || workspace_bytes < plan.workspace_bytes) {
+        if (workspace)
+            return fail(AA_ERR_INVALID_ARGUMENT, "aa_anchor_attention_groups: workspace too small");
+        AA_CUDA(tmp.alloc(plan.workspace_bytes));
+        workspace = tmp.p;
+    }
+    const Layout L = carve(*p, plan, workspace);
+    return fused_fast(p, plan, L, q, k, v, zero_anchor, out, out_dtype, computed, st, group_begin,
+                      group_end);
 }
 
 aa_status aa_set_stage_events(void* const* events, int count) {

@@ -23,14 +23,14 @@ namespace {
 constexpr int kCompactWarps = AA_COMPACT_WARPS;
 
 __global__ void __launch_bounds__(kCompactWarps * 32)
-    k_compact(Geo geo, int64_t hq, const uint32_t* __restrict__ bits, int64_t words_per_row,
-              const int64_t* __restrict__ offsets, int64_t cap, uint32_t* __restrict__ indices,
-              int32_t* __restrict__ counts) {
+    k_compact(Geo geo, int64_t hq, int64_t g_end, const uint32_t* __restrict__ bits,
+              int64_t words_per_row, const int64_t* __restrict__ offsets, int64_t cap,
+              uint32_t* __restrict__ indices, int32_t* __restrict__ counts) {
     __shared__ uint32_t stage[kCompactWarps][1024];
     __shared__ int run_excl[kCompactWarps + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t groups = geo.groups();
-    const int64_t g = groups - 1 - blockIdx.x / hq, h = blockIdx.x % hq;
+    const int64_t g = g_end - 1 - blockIdx.x / hq, h = blockIdx.x % hq;
     const int64_t len = geo.middle_len(g);
     const int64_t words = (len + 31) >> 5;
     const uint32_t* row = bits + (h * groups + g) * words_per_row;
@@ -90,12 +90,12 @@ __global__ void __launch_bounds__(kCompactWarps * 32)
     }
 }
 
-__global__ void k_computed(Geo geo, int64_t covered, const int32_t* __restrict__ counts,
-                           int64_t* __restrict__ computed) {
+__global__ void k_computed(Geo geo, int64_t g0, int64_t g1, int64_t covered,
+                           const int32_t* __restrict__ counts, int64_t* __restrict__ computed) {
     const int64_t h = blockIdx.x;
     const int64_t groups = geo.groups();
     long long s = 0;
-    for (int64_t g = threadIdx.x; g < groups; g += blockDim.x)
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x)
         s += static_cast<long long>(counts[h * groups + g]) * (geo.row_end(g) - geo.row_begin(g));
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -217,17 +217,20 @@ cudaError_t launch_offsets(const Geo& geo, int64_t* offsets, cudaStream_t s) {
 
 cudaError_t launch_compact(const Geo& geo, int64_t hq, const uint32_t* bits,
                            int64_t words_per_row, const int64_t* offsets, int64_t cap,
-                           uint32_t* indices, int32_t* counts, cudaStream_t s) {
-    const int64_t rows = geo.groups() * hq;
-    if (rows == 0) return cudaSuccess;
-    k_compact<<<static_cast<unsigned>(rows), kCompactWarps * 32, 0, s>>>(geo, hq, bits, words_per_row,
+                           uint32_t* indices, int32_t* counts, cudaStream_t s, int64_t g0,
+                           int64_t g1) {
+    if (g1 < 0) g1 = geo.groups();
+    const int64_t rows = (g1 - g0) * hq;
+    if (rows <= 0) return cudaSuccess;
+    k_compact<<<static_cast<unsigned>(rows), kCompactWarps * 32, 0, s>>>(geo, hq, g1, bits, words_per_row,
                                                                         offsets, cap, indices, counts);
     return cudaGetLastError();
 }
 
 cudaError_t launch_computed(const Geo& geo, int64_t hq, int64_t covered, const int32_t* counts,
-                            int64_t* computed, cudaStream_t s) {
-    k_computed<<<static_cast<unsigned>(hq), 32, 0, s>>>(geo, covered, counts, computed);
+                            int64_t* computed, cudaStream_t s, int64_t g0, int64_t g1) {
+    if (g1 < 0) g1 = geo.groups();
+    k_computed<<<static_cast<unsigned>(hq), 32, 0, s>>>(geo, g0, g1, covered, counts, computed);
     return cudaGetLastError();
 }
 

@@ -15,6 +15,9 @@ struct FastArgs {
     int64_t hq, hkv, rep;
     int64_t q_rs, q_hs, kv_rs, kv_hs;  // element strides (bf16 elements)
     double theta;
+    // query groups computed: [g0, g1) (default all); rows of other groups
+    // are neither read (q) nor written (state, lists, out)
+    int64_t g0, g1;
 };
 
 // Records stage event i of aa_set_stage_events on `st` (no-op when unset).

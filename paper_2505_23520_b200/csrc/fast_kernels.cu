@@ -112,6 +112,7 @@ struct FaParams {
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
     int item0;    // first work item of this launch (K3 split launches)
+    int g_end;    // work items cover groups [g_end - grid groups, g_end)
     // K1 -> K3 hand-off format: 0 = acc f32 unnormalised (AnchorState::acc,
     // the stage API); 1 = f16 acc / l (normalised, |.| <= max|v|: half the
     // bytes both ways; the fused chain)
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // siblings select mostly the same keys), so the gathers hit L2.
     const int ipg = (P.step + 1) / 2;  // query-block pairs per group
     const int L = blockIdx.x + P.item0;
-    const int gi = P.groups - 1 - L / (ipg * P.hq);
+    const int gi = P.g_end - 1 - L / (ipg * P.hq);
     const int rem = L % (ipg * P.hq);
     const int h = rem / ipg;
     const int pi = ipg - 1 - rem % ipg;
@@ -1039,13 +1040,13 @@ struct IdSmem {
 struct IdWork {
     Geo geo;
     int rep, n_mt, n_pairs, J;
+    int g0, gr;  // A-operand rows cover groups [g0, g0 + gr)
 };
 
 // Key tiles of M-tile mt: up to the widest middle region of its groups.
 __device__ __forceinline__ int id_tiles(const IdWork& w, int mt) {
     if (mt >= w.n_mt) return 0;
-    const int groups = static_cast<int>(w.geo.groups());
-    const int g_last = min(groups - 1, ((mt + 1) * kB - 1) / w.rep);
+    const int g_last = w.g0 + min(w.gr - 1, ((mt + 1) * kB - 1) / w.rep);
     const int64_t span = w.geo.middle_end(g_last) - w.geo.b_kv;
     return span > 0 ? static_cast<int>((span + kB - 1) / kB) : 0;
 }
@@ -1174,8 +1175,8 @@ __global__ void __launch_bounds__(kIdThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const int Tm = m ? T1 : T0;
         const int grow = (mt0 + m) * kB + r;
-        const int g = grow / w.rep, hh = kvh * w.rep + grow % w.rep;
-        const bool valid = grow < groups * w.rep;
+        const int g = w.g0 + grow / w.rep, hh = kvh * w.rep + grow % w.rep;
+        const bool valid = grow < w.gr * w.rep;
         int64_t mend = 0;
         float thr = 0.f;
         if (valid) {
@@ -1239,16 +1240,17 @@ __global__ void __launch_bounds__(kIdThreads, 1)
     PROF(if (threadIdx.x == 0) { atomicAdd(&g_prof[5][6], clock64() - t_cta0); atomicAdd(&g_prof[5][7], 1ull); })
 }
 
-// q_bar (f32 [hq, G, d]) -> A operand rows r = g*rep + hh of KV head kvh as a
-// two-term bf16 split: out[(2*kvh + 0), r, :] = hi, out[(2*kvh + 1), r, :] = lo.
-__global__ void k_split_qbar(int groups, int rep, int rows_pad, const float* __restrict__ qbar,
-                             __nv_bfloat16* __restrict__ out) {
+// q_bar (f32 [hq, G, d]) -> A operand rows r = (g - g0)*rep + hh of KV head kvh
+// (groups [g0, g0 + gr)) as a two-term bf16 split: out[(2*kvh + 0), r, :] = hi,
+// out[(2*kvh + 1), r, :] = lo.
+__global__ void k_split_qbar(int groups, int g0, int gr, int rep, int rows_pad,
+                             const float* __restrict__ qbar, __nv_bfloat16* __restrict__ out) {
     const int kvh = blockIdx.y;
     const int r = blockIdx.x;
     const int t = threadIdx.x;
     float x = 0.f;
-    if (r < groups * rep) {
-        const int g = r / rep, hh = kvh * rep + r % rep;
+    if (r < gr * rep) {
+        const int g = g0 + r / rep, hh = kvh * rep + r % rep;
         x = qbar[(static_cast<int64_t>(hh) * groups + g) * kD + t];
     }
     const __nv_bfloat16 hi = __float2bfloat16(x);
@@ -1259,12 +1261,12 @@ __global__ void k_split_qbar(int groups, int rep, int rows_pad, const float* __r
 
 // Pooled query / anchor per group from K1's per-query-block partials
 // (avgpool_rows / avgpool_vector, R/src/matrix.cpp:44-81).  grid (G, hq).
-__global__ void k_pool_fast(Geo geo, int64_t q_rs, int64_t q_hs, const __nv_bfloat16* __restrict__ q,
-                            const float* __restrict__ m, const float* __restrict__ qsum,
-                            const double* __restrict__ msum, double* __restrict__ anchor,
-                            float* __restrict__ qbar) {
-    const int64_t g = blockIdx.x, h = blockIdx.y;
-    const int64_t groups = gridDim.x, T = geo.q_blocks();
+__global__ void k_pool_fast(Geo geo, int64_t g0, int64_t q_rs, int64_t q_hs,
+                            const __nv_bfloat16* __restrict__ q, const float* __restrict__ m,
+                            const float* __restrict__ qsum, const double* __restrict__ msum,
+                            double* __restrict__ anchor, float* __restrict__ qbar) {
+    const int64_t g = g0 + blockIdx.x, h = blockIdx.y;
+    const int64_t groups = geo.groups(), T = geo.q_blocks();
     const int64_t rb = geo.row_begin(g), re = geo.row_end(g);
     const int64_t qb0 = g * geo.step, qb1 = min(T, (g + 1) * geo.step);
     const double inv = 1.0 / static_cast<double>(re - rb);
@@ -1485,7 +1487,8 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     static unsigned long long attr_done = 0;  // per MODE instantiation, bit per device
     if ((e = smem_attr_once(fa_pair<MODE>, static_cast<int>(kSmemBytes), &attr_done))) return e;
     const int ipg = (P.step + 1) / 2;
-    const unsigned grid = static_cast<unsigned>(P.groups * ipg * f.hq);
+    P.g_end = static_cast<int>(f.g1);
+    const unsigned grid = static_cast<unsigned>((f.g1 - f.g0) * ipg * f.hq);
     P.cluster = 1;
     // K3: cluster the pairs of one (head, group) so each gathered tile is
     // fetched once per cluster (TMA multicast); needs every group complete
@@ -1555,8 +1558,8 @@ cudaError_t fast_anchor(const FastArgs& f, const void* q, const void* k, const v
 
 cudaError_t fast_pool(const FastArgs& f, const void* q, const float* m, const float* qsum,
                       const double* msum, double* anchor, float* qbar, cudaStream_t s) {
-    k_pool_fast<<<dim3(static_cast<unsigned>(f.geo.groups()), static_cast<unsigned>(f.hq)), 128, 0,
-                  s>>>(f.geo, f.q_rs, f.q_hs, static_cast<const __nv_bfloat16*>(q), m, qsum, msum,
+    k_pool_fast<<<dim3(static_cast<unsigned>(f.g1 - f.g0), static_cast<unsigned>(f.hq)), 128, 0,
+                  s>>>(f.geo, f.g0, f.q_rs, f.q_hs, static_cast<const __nv_bfloat16*>(q), m, qsum, msum,
                        anchor, qbar);
     return cudaGetLastError();
 }
@@ -1571,12 +1574,13 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
                           const double* anchor, uint32_t* bits, int64_t words_per_row,
                           cudaStream_t s, void* scratch, size_t scratch_bytes) {
     const int64_t G = f.geo.groups();
-    const int64_t max_end = f.geo.middle_end(G - 1);
+    const int64_t Gr = f.g1 - f.g0;
+    const int64_t max_end = f.geo.middle_end(f.g1 - 1);
     const int64_t span = max_end > f.geo.b_kv ? max_end - f.geo.b_kv : 0;
     const int64_t tiles = (span + kB - 1) / kB;
     if (tiles == 0) return cudaSuccess;
     if (words_per_row % 4) return cudaErrorInvalidValue;  // 16-byte word stores
-    const int rows = static_cast<int>(G * f.rep);
+    const int rows = static_cast<int>(Gr * f.rep);
     const int rows_pad = (rows + kB - 1) / kB * kB;
     void* split = scratch;
     cudaError_t e;
@@ -1584,8 +1588,8 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     const bool own = scratch == nullptr || scratch_bytes < split_bytes;
     if (own && (e = cudaMallocAsync(&split, split_bytes, s))) return e;
     k_split_qbar<<<dim3(static_cast<unsigned>(rows_pad), static_cast<unsigned>(f.hkv)), kD, 0, s>>>(
-        static_cast<int>(G), static_cast<int>(f.rep), rows_pad, qbar,
-        static_cast<__nv_bfloat16*>(split));
+        static_cast<int>(G), static_cast<int>(f.g0), static_cast<int>(Gr), static_cast<int>(f.rep), rows_pad,
+        qbar, static_cast<__nv_bfloat16*>(split));
     CUtensorMap ta, tk;
     if ((e = make_map_3d(&ta, split, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rows_pad, 2 * f.hkv, kD,
                          static_cast<int64_t>(rows_pad) * kD)) ||
@@ -1609,6 +1613,8 @@ cudaError_t fast_identify(const FastArgs& f, const void* k, const float* qbar,
     w.rep = static_cast<int>(f.rep);
     w.n_mt = rows_pad / kB;
     w.n_pairs = (w.n_mt + 1) / 2;
+    w.g0 = static_cast<int>(f.g0);
+    w.gr = static_cast<int>(Gr);
     const int heads_pairs = static_cast<int>(f.hkv) * w.n_pairs;
     const int nchunks = static_cast<int>((tiles + kIdChunk - 1) / kIdChunk);
     w.J = std::max(1, std::min(nchunks, (sms > 0 ? sms : 148) / std::max(1, heads_pairs)));

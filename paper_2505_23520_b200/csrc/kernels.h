@@ -42,13 +42,16 @@ cudaError_t launch_recall_exact(const ExactArgs& a, const float* q, const float*
 // ---- shared (common_kernels.cu) ----
 // Ordered stream compaction of the per-(head, group) selection bitmask into
 // the capacity-layout index lists (ballot/popc + block scan).
+// Rows of groups [g0, g1) (g1 < 0: all groups).
 cudaError_t launch_compact(const Geo& geo, int64_t hq, const uint32_t* bits,
                            int64_t words_per_row, const int64_t* offsets, int64_t cap,
-                           uint32_t* indices, int32_t* counts, cudaStream_t s);
+                           uint32_t* indices, int32_t* counts, cudaStream_t s, int64_t g0 = 0,
+                           int64_t g1 = -1);
 // RunStats::computed_positions per head = covered + sum_g counts[h,g]*rows(g)
 // (R/tests/test_sparse_exec.cpp:106-121 accounting identity).
+// (over groups [g0, g1); covered = the anchor positions of those rows)
 cudaError_t launch_computed(const Geo& geo, int64_t hq, int64_t covered, const int32_t* counts,
-                            int64_t* computed, cudaStream_t s);
+                            int64_t* computed, cudaStream_t s, int64_t g0 = 0, int64_t g1 = -1);
 // offsets[g] = stripe_offset(g) for g in [0, groups] (capacity layout).
 cudaError_t launch_offsets(const Geo& geo, int64_t* offsets, cudaStream_t s);
 // Stage-API list check / filter (see k_filter_lists): folded entries of each
