@@ -185,7 +185,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     const int pi = ipg - 1 - rem % ipg;
     const int kvh = h / P.rep;
     const int qA = gi * P.step + 2 * pi;
-    if (qA >= P.T_m) return;
+    // K3 cluster mode: a pair past the last query block of a partial group
+    // still walks the group's stripe tiles (it gathers its share of every
+    // multicast tile for its peer) on a query tile that lies wholly past n —
+    // TMA zero-fills it and every store of it is clipped / masked by row < n.
+    // Otherwise such a CTA has no work.
+    if (qA >= P.T_m && !(MODE == SPARSE && P.cluster > 1)) return;
     const bool hasB = (2 * pi + 1 < P.step) && (qA + 1 < P.T_m);
     const int qB = qA + 1;
 
@@ -1491,12 +1496,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     const unsigned grid = static_cast<unsigned>((f.g1 - f.g0) * ipg * f.hq);
     P.cluster = 1;
     // K3: cluster the pairs of one (head, group) so each gathered tile is
-    // fetched once per cluster (TMA multicast); needs every group complete
-    // (no early-exiting CTA) and the pairs of a group to fill whole clusters.
+    // fetched once per cluster (TMA multicast); needs the pairs of a group to
+    // fill whole clusters (pairs past the end of a partial last group run as
+    // gather-only members, see fa_pair).
     // Measured with split K / V gather warps (128k Llama): clusters of 2 /
     // 4 -> K3 16.3-16.4 / 17.1-17.3 ms (4-CTA clusters co-schedule on only
     // 132 of 148 SMs); AA_K3_CLUSTER overrides.
-    if (MODE == SPARSE && P.T_m % P.step == 0) {
+    if (MODE == SPARSE) {
         int want = 2;
         if (const char* env = getenv("AA_K3_CLUSTER")) want = atoi(env);
         for (int c : {want, 2, 1})

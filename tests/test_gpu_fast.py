@@ -85,7 +85,9 @@ def test_anchor_pass_matches_oracle(oracle, n, step):
 
 
 @pytest.mark.parametrize("n,step,theta", [(4096, 16, 12.0), (2048, 2, 12.0), (4000, 4, 13.0),
-                                          (8192, 16, 10.0), (1100, 1, 14.0)])
+                                          (8192, 16, 10.0), (1100, 1, 14.0),
+                                          # ragged last groups (K3 clusters with gather-only pairs)
+                                          (5000, 16, 12.0), (6444, 16, 11.0), (2300, 2, 12.0)])
 def test_pipeline_matches_oracle(oracle, n, step, theta):
     c = capi()
     q, k, v = gen(n, seed=7 * n + step)
