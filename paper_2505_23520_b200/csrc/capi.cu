@@ -90,7 +90,9 @@ Layout carve(const aa_problem& p, const aa_plan& plan, void* ws) {
     L.words_per_row = words_per_row(p.n);
     L.m = c.take(hq * n * se);
     L.l = c.take(hq * n * se);
-    L.acc = c.take(hq * n * d * se);
+    // the fused fast chain hands K1's state to K3 as f16 acc / l (half the
+    // bytes of the f32 AnchorState::acc the stage API returns)
+    L.acc = c.take(hq * n * d * (p.dtype == AA_BF16 ? 2 : se));
     L.qsum = c.take(hq * T * d * 4);
     L.msum = c.take(hq * T * 8);
     L.anchor = c.take(hq * G * 8);
