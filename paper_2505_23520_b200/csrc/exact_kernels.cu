@@ -165,6 +165,10 @@ __global__ void k_identify_exact(ExactArgs a, const float* __restrict__ k,
 // --------------------------------------------------------------- Alg. 3 --
 // R/src/sparse_exec.cpp:13-124.  grid (n, hq), block 32,
 // smem chunk*(f64 + u32) + d*f64.
+// Scores staged in shared memory per fold chunk up to this many entries;
+// longer FoldPlan chunks fold in two passes (same values, same order).
+constexpr int64_t kSparseStage = 4096;
+
 __global__ void k_sparse_exact(ExactArgs a, const float* __restrict__ q,
                                const float* __restrict__ k, const float* __restrict__ v,
                                const double* __restrict__ m_in, const double* __restrict__ l_in,
@@ -177,7 +181,7 @@ __global__ void k_sparse_exact(ExactArgs a, const float* __restrict__ q,
     extern __shared__ double smem[];
     double* acc = smem;
     double* qk = smem + a.d;
-    uint32_t* kept = reinterpret_cast<uint32_t*>(qk + chunk);
+    uint32_t* kept = reinterpret_cast<uint32_t*>(qk + (chunk > kSparseStage ? 0 : chunk));
     const int lane = threadIdx.x;
     const int64_t i = blockIdx.x, h = blockIdx.y;
     const Geo& G = a.geo;
@@ -197,6 +201,56 @@ __global__ void k_sparse_exact(ExactArgs a, const float* __restrict__ q,
         const int64_t c1 = c0 + chunk < cnt ? c0 + chunk : cnt;
         int64_t taken = 0;
         double cmax = -INFINITY;
+        if (chunk > kSparseStage) {
+            // chunks longer than the staging buffer: pass 1 takes the chunk max
+            // and count, pass 2 recomputes each kept score (the same f64 dot in
+            // the same order, so the same value) and folds it in list order —
+            // bit-identical to the staged fold below, for any FoldPlan chunk
+            for (int64_t s0 = c0; s0 < c1; s0 += 32) {
+                const int64_t s = s0 + lane;
+                bool keep = false;
+                uint32_t j = 0;
+                if (s < c1) {
+                    j = list[s];
+                    keep = !(static_cast<int64_t>(j) > i) &&
+                           !(static_cast<int64_t>(j) < G.b_kv || static_cast<int64_t>(j) >= wstart);
+                }
+                if (keep)
+                    cmax = fmax(cmax, dot_f64(qr, kb + static_cast<int64_t>(j) * a.kv_rs, d) * a.inv_sqrt_d);
+                taken += __popc(__ballot_sync(0xffffffffu, keep));
+            }
+            cmax = warp_max(cmax);
+            if (taken == 0) continue;
+            taken_total += static_cast<unsigned long long>(taken);
+            const double m_new = fmax(mi, cmax);
+            const double alpha = exp(mi - m_new);
+            for (int64_t t = lane; t < d; t += 32) acc[t] *= alpha;
+            double lc = 0.0;
+            for (int64_t s0 = c0; s0 < c1; s0 += 32) {
+                const int64_t s = s0 + lane;
+                bool keep = false;
+                uint32_t j = 0;
+                double sc = 0.0;
+                if (s < c1) {
+                    j = list[s];
+                    keep = !(static_cast<int64_t>(j) > i) &&
+                           !(static_cast<int64_t>(j) < G.b_kv || static_cast<int64_t>(j) >= wstart);
+                }
+                if (keep) sc = dot_f64(qr, kb + static_cast<int64_t>(j) * a.kv_rs, d) * a.inv_sqrt_d;
+                for (uint32_t bal = __ballot_sync(0xffffffffu, keep); bal; bal &= bal - 1) {
+                    const int src = __ffs(bal) - 1;
+                    const double p = exp(__shfl_sync(0xffffffffu, sc, src) - m_new);
+                    const uint32_t jj = __shfl_sync(0xffffffffu, j, src);
+                    lc += p;
+                    const float* vr = vb + static_cast<int64_t>(jj) * a.kv_rs;
+                    for (int64_t t = lane; t < d; t += 32) acc[t] += p * static_cast<double>(vr[t]);
+                }
+            }
+            li = li * alpha + lc;
+            mi = m_new;
+            __syncwarp();
+            continue;
+        }
         for (int64_t s0 = c0; s0 < c1; s0 += 32) {
             const int64_t s = s0 + lane;
             bool keep = false;
@@ -390,10 +444,9 @@ cudaError_t launch_sparse_exact(const ExactArgs& a, const float* q, const float*
                                 const int64_t* offsets, int64_t cap, bool csr, int64_t chunk,
                                 void* out, aa_dtype out_dtype, unsigned long long* computed,
                                 cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(a.d) * 8 + static_cast<size_t>(chunk) * 12;
+    const int64_t staged = chunk > kSparseStage ? 0 : chunk;
+    const size_t smem = static_cast<size_t>(a.d) * 8 + static_cast<size_t>(staged) * 12;
     if (smem > 48 * 1024) {
-        // beyond 227 KB (index_chunk above ~19k with lists that long) the
-        // launch is refused with the attribute's error
         const cudaError_t e = cudaFuncSetAttribute(
             k_sparse_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;

@@ -67,10 +67,18 @@ def test_fold_plans_do_not_change_result(aa):
     idx = aa.identify_stripes_from_state(w, st, cfg)
     assert idx.total_selected() > 0
     base, bstats = aa.sparse_attention(w, st, idx, cfg)
-    for chunk, seed in [(1, 0), (7, 1), (64, 2), (1000, 3), (13, 99)]:
+    for chunk, seed in [(1, 0), (7, 1), (64, 2), (1000, 3), (13, 99), (5000, 4), (10**6, 5)]:
         alt, astats = aa.sparse_attention(w, st, idx, cfg, aa.FoldPlan(chunk, seed))
         assert np.abs(base - alt).max() <= 1e-6
         assert astats.computed_positions == bstats.computed_positions
+    # chunks longer than the kernel's score staging (4096) fold in two passes
+    # with the same scores in the same order: bit-identical to one staged chunk
+    longest = max(len(g) for g in idx.groups)
+    assert longest <= 4096
+    staged, _ = aa.sparse_attention(w, st, idx, cfg, aa.FoldPlan(4096, 0))
+    for chunk in (4097, 10**6):
+        two_pass, _ = aa.sparse_attention(w, st, idx, cfg, aa.FoldPlan(chunk, 0))
+        assert np.array_equal(staged, two_pass), chunk
 
 
 def test_covered_stripes_are_skipped(aa, oracle):
