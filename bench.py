@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-samples", type=int, default=3,
+    ap.add_argument("--cpu-samples", type=int, default=6,
                     help="sparse_attention sample steps of the cpu_baseline reference timing")
     ap.add_argument("--no-dense-libs", action="store_true",
                     help="skip the cuDNN / flashinfer dense comparators")

@@ -59,6 +59,14 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef AA_POLY_PAIRS
 #define AA_POLY_PAIRS 0
 #endif
+// K3 work order: 1 = KV-head-major (every item of one KV head — its groups
+// heavy-first, then its query heads, then pairs — before the next KV head's),
+// so the ~74 clusters running at once gather from one KV head's K / V rows
+// and find them in L2: K3 DRAM read 5.06 -> 2.44 GB per layer, L2 hit rate
+// 73.7 -> 82.7% (ncu, 128k Llama).  0 = group-major over all heads.
+#ifndef AA_K3_KV_MAJOR
+#define AA_K3_KV_MAJOR 1
+#endif
 #ifndef AA_POLY_PAIRS_K1
 #define AA_POLY_PAIRS_K1 4
 #endif
@@ -112,7 +120,8 @@ struct FaParams {
     int out_bf16;
     int cluster;  // K3: CTAs per cluster sharing gathered tiles (1 = none)
     int item0;    // first work item of this launch (K3 split launches)
-    int g_end;    // work items cover groups [g_end - grid groups, g_end)
+    int g_end;    // work items cover groups [g_end - n_groups, g_end)
+    int n_groups;
     // K1 -> K3 hand-off format: 0 = acc f32 unnormalised (AnchorState::acc,
     // the stage API); 1 = f16 acc / l (normalised, |.| <= max|v|: half the
     // bytes both ways; the fused chain)
@@ -176,13 +185,34 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // work item: heavy-first (last groups first).  Within a group, the pairs of
     // one head are adjacent, then the heads of one KV head: CTAs that run
     // together gather the same stripe rows (one list per (head, group); GQA
-    // siblings select mostly the same keys), so the gathers hit L2.
+    // siblings select mostly the same keys), so the gathers hit L2.  K3 goes
+    // further and runs one KV head's items at a time (AA_K3_KV_MAJOR).
     const int ipg = (P.step + 1) / 2;  // query-block pairs per group
     const int L = blockIdx.x + P.item0;
+#if AA_K3_KV_MAJOR
+    // K3: KV-head-major — all of one KV head's items (heavy groups first,
+    // then its query heads, then pairs) before the next KV head's, so the
+    // CTAs running at once gather from one KV head's K/V (L2-resident)
+    int gi, h, pi;
+    if (MODE == SPARSE) {
+        const int per_kv = P.n_groups * P.rep * ipg;
+        const int kvb = L / per_kv, r2 = L % per_kv;
+        gi = P.g_end - 1 - r2 / (P.rep * ipg);
+        const int r3 = r2 % (P.rep * ipg);
+        h = kvb * P.rep + r3 / ipg;
+        pi = ipg - 1 - r3 % ipg;
+    } else {
+        gi = P.g_end - 1 - L / (ipg * P.hq);
+        const int rem = L % (ipg * P.hq);
+        h = rem / ipg;
+        pi = ipg - 1 - rem % ipg;
+    }
+#else
     const int gi = P.g_end - 1 - L / (ipg * P.hq);
     const int rem = L % (ipg * P.hq);
     const int h = rem / ipg;
     const int pi = ipg - 1 - rem % ipg;
+#endif
     const int kvh = h / P.rep;
     const int qA = gi * P.step + 2 * pi;
     // K3 cluster mode: a pair past the last query block of a partial group
@@ -1493,6 +1523,7 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
     if ((e = smem_attr_once(fa_pair<MODE>, static_cast<int>(kSmemBytes), &attr_done))) return e;
     const int ipg = (P.step + 1) / 2;
     P.g_end = static_cast<int>(f.g1);
+    P.n_groups = static_cast<int>(f.g1 - f.g0);
     const unsigned grid = static_cast<unsigned>((f.g1 - f.g0) * ipg * f.hq);
     P.cluster = 1;
     // K3: cluster the pairs of one (head, group) so each gathered tile is
