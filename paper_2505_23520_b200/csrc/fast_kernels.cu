@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 for (int kk = 0; kk < 8; ++kk)
                     mma_ts_w(tO, tS + kk * 8, kDescHi | (lv + kk * (2048 >> 4)), kIdescPV,
                            (j > 0 || kk > 0) ? 1u : 0u);
-                mma_commit_w(&S.bar_o_done[X]);
+                // O_X is read only by the epilogue: one completion, after the last PV
+                if (j + 1 == (X ? nB : nA)) mma_commit_w(&S.bar_o_done[X]);
             };
             // a stage is released to every producer of the cluster that fills it
             auto release = [&](uint64_t* bar) {
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     pv(1, j);
                     if (j + 1 < nB) qk(1, j + 1);
                 }
-                release(&S.bar_v_empty[j & 1]);
+                if (!kQkOnly<MODE>) release(&S.bar_v_empty[j & 1]);  // no V ring in the QK-only passes
                 if (j + 1 < ntiles) release(&S.bar_k_empty[(j + 1) % kKStages]);
             }
             if (C > 1) {
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     }
             }
             if (nX > 0) {
-                mbar_wait(&S.bar_o_done[X], (nX - 1) & 1);
+                mbar_wait(&S.bar_o_done[X], 0);
                 tc_fence_after();
             }
             PROF(if (lane == 0 && warp == 4) atomicAdd(&g_prof[MODE][13], clock64() - t_epi0);)
