@@ -59,6 +59,19 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef AA_POLY_PAIRS
 #define AA_POLY_PAIRS 0
 #endif
+// K3: warps issuing the K-row gathers (1: warp 0; 2: warps 0 and 2, one
+// column half each)
+#ifndef AA_K3_KGATHER_WARPS
+#define AA_K3_KGATHER_WARPS 2
+#endif
+constexpr int kKGatherWarps = AA_K3_KGATHER_WARPS;
+// K3: warps issuing the V-row gathers (1: warp 3; 2: warps 3 and 12, one column
+// half each — the CTA then has a fourth warpgroup, warps 12-15, and the
+// softmax warpgroups 208 instead of 224 registers per thread)
+#ifndef AA_K3_VGATHER_WARPS
+#define AA_K3_VGATHER_WARPS 2
+#endif
+constexpr int kVGatherWarps = AA_K3_VGATHER_WARPS;
 // K3 work order: 1 = KV-head-major (every item of one KV head — its groups
 // heavy-first, then its query heads, then pairs — before the next KV head's),
 // so the ~74 clusters running at once gather from one KV head's K / V rows
@@ -92,6 +105,10 @@ enum Mode { ANCHOR = 0, SPARSE = 1, DENSE = 2, RECALL = 3, TILEMASS = 4 };
 
 template <int MODE>
 constexpr bool kQkOnly = MODE == RECALL || MODE == TILEMASS;
+template <int MODE>
+constexpr bool kWideK3 = MODE == SPARSE && kVGatherWarps == 2;
+template <int MODE>
+constexpr int kThreadsOf = kWideK3<MODE> ? 512 : kPairThreads;
 
 struct FaParams {
     int n, hq, rep, T_m, step;
@@ -170,7 +187,7 @@ __device__ __forceinline__ int kv_tile_of(int mode, int it, int wsb) {
 // ping-pong); tcgen05 MMAs of one thread execute in issue order, so QK_X(j+1)
 // overwriting S_X after PV_X(j) has read P_X is ordered by the pipe.
 template <int MODE>
-__global__ void __launch_bounds__(kPairThreads, 1)
+__global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
     fa_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKg,
             const __grid_constant__ CUtensorMap tmVg, const FaParams P) {
@@ -305,7 +322,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         }
     };
     int pre_r[4] = {0, 0, 0, 0};
-    if (MODE == SPARSE && ntiles > 0 && (warp == 0 || warp == 3)) stripe_rows(0, warp == 0, pre_r);
+    if (MODE == SPARSE && ntiles > 0 && (warp == 0 || warp == 2 || warp == 3 || warp == 12))
+        stripe_rows(0, warp == 0 || warp == 2, pre_r);
     if (warp == 1) tmem_alloc(&S.tmem_base, 512);
     tc_fence_before();
     if (C > 1) cluster_sync(); else __syncthreads();
@@ -318,7 +336,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // every stripe tile (gather4: 4 rows x 128 B per instruction, x 2 column
     // halves); in a cluster of C each CTA gathers rows [crank*128/C, +128/C)
     // of a tile and multicasts them to the C CTAs.
-    auto gather_split = [&](bool isK) {
+    // halves: 3 = both column halves of every row; 1 / 2 = only the first /
+    // second 64 columns (two warps share one operand's gathers: a warp issues
+    // its lanes' gather4 ops one after another, ~70-90 cycles each, so the
+    // issue rate scales with the number of issuing warps —
+    // profiles/probes/gather4_rate.txt).  The warp owning half 0 arms the
+    // stage's full barrier for the whole tile.
+    auto gather_split = [&](bool isK, int halves) {
         const bool gl = lane < g_lanes;
         int r[4] = {pre_r[0], pre_r[1], pre_r[2], pre_r[3]};
         for (int it = 0; it < ntiles; ++it) {
@@ -329,18 +353,18 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             uint64_t* empty = isK ? &S.bar_k_empty[st] : &S.bar_v_empty[st];
             if (lane == 0) {
                 if (it >= depth) mbar_wait(empty, (ph - 1) & 1);
-                mbar_expect_tx(full, kTileBytes);
+                if (halves & 1) mbar_expect_tx(full, kTileBytes);
             }
             __syncwarp();
             uint8_t* dst = (isK ? S.k[st] : S.v[st]) + g_row0 * 128;
             const CUtensorMap* tm = isK ? &tmKg : &tmVg;
             if (gl) {
                 if (C > 1) {
-                    tma_gather4_mc(dst, tm, full, cmask, 0, r[0], r[1], r[2], r[3]);
-                    tma_gather4_mc(dst + kAtomBytes, tm, full, cmask, 64, r[0], r[1], r[2], r[3]);
+                    if (halves & 1) tma_gather4_mc(dst, tm, full, cmask, 0, r[0], r[1], r[2], r[3]);
+                    if (halves & 2) tma_gather4_mc(dst + kAtomBytes, tm, full, cmask, 64, r[0], r[1], r[2], r[3]);
                 } else {
-                    tma_gather4(dst, tm, full, 0, r[0], r[1], r[2], r[3]);
-                    tma_gather4(dst + kAtomBytes, tm, full, 64, r[0], r[1], r[2], r[3]);
+                    if (halves & 1) tma_gather4(dst, tm, full, 0, r[0], r[1], r[2], r[3]);
+                    if (halves & 2) tma_gather4(dst + kAtomBytes, tm, full, 64, r[0], r[1], r[2], r[3]);
                 }
             }
             if (it + 1 < ntiles) stripe_rows(it + 1, isK, r);  // next tile's rows, ahead of its stage
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         // ------------------------------------------------------------ producer
         // (the Q pair and the first contiguous K / V tile were issued at init)
         if (MODE == SPARSE) {
-            gather_split(true);  // V rows: warp 3
+            gather_split(true, kKGatherWarps == 2 ? 1 : 3);  // K rows (warp 2: the second half)
         } else if (MODE != SPARSE) {
             for (int it = 1; it < ntiles; ++it) {
                 if (lane == 0) {
@@ -454,7 +478,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         __syncwarp();
     } else if (warp < 4) {
         setmaxnreg_dec<56>();  // warp 3: K3's V-row gathers; warps 2-3: K1's column sums
-        if (MODE == SPARSE && warp == 3) gather_split(false);
+        if (MODE == SPARSE && warp == 3) gather_split(false, kWideK3<MODE> ? 1 : 3);
+        if (MODE == SPARSE && kKGatherWarps == 2 && warp == 2) gather_split(true, 2);
         if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
             // pooled-query partials (avgpool_rows, R/src/matrix.cpp:44-65): column
             // sums of each query tile over its 128 rows (TMA zero-fills rows past
@@ -479,8 +504,14 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             }
             mbar_arrive(&S.bar_qsum);  // the epilogue reuses the Q tiles as staging
         }
+    } else if (kWideK3<MODE> && warp >= 12) {
+        setmaxnreg_dec<40>();  // K3's fourth warpgroup: the second half of the V-row gathers
+        // (warps 13-15 stay idle: more issuing / polling warps measured slower,
+        // profiles/r2_experiments)
+        if (warp == 12) gather_split(false, 2);
     } else {
-        setmaxnreg_inc<224>();
+        if constexpr (kWideK3<MODE>) setmaxnreg_inc<208>();
+        else setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
         const int nX = X ? nB : nA;
@@ -1544,13 +1575,13 @@ cudaError_t launch_fa(const FastArgs& f, const void* q, const void* k, const voi
             }
     }
     if (P.cluster == 1) {
-        fa_pair<MODE><<<grid, kPairThreads, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
+        fa_pair<MODE><<<grid, kThreadsOf<MODE>, kSmemBytes, s>>>(tq, tk, tv, tkg, tvg, P);
         return cudaGetLastError();
     }
     auto launch_cluster = [&](const FaParams& PP, unsigned g, cudaStream_t st) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(g);
-        cfg.blockDim = dim3(kPairThreads);
+        cfg.blockDim = dim3(kThreadsOf<MODE>);
         cfg.dynamicSmemBytes = kSmemBytes;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
