@@ -109,6 +109,24 @@ template <int MODE>
 constexpr bool kWideK3 = MODE == SPARSE && kVGatherWarps == 2;
 template <int MODE>
 constexpr int kThreadsOf = kWideK3<MODE> ? 512 : kPairThreads;
+// register split of the wide K3 CTA (per thread; 128 x role + 128 x wg3 +
+// 256 x softmax <= 65536): role warpgroup (MMA + gathers), fourth warpgroup,
+// softmax warpgroups
+#ifndef AA_K3_REGS_ROLE
+#define AA_K3_REGS_ROLE 56
+#endif
+#ifndef AA_K3_REGS_WG3
+#define AA_K3_REGS_WG3 40
+#endif
+#ifndef AA_K3_REGS_SOFTMAX
+#define AA_K3_REGS_SOFTMAX 208
+#endif
+constexpr int kWideRegs[3] = {AA_K3_REGS_ROLE, AA_K3_REGS_WG3, AA_K3_REGS_SOFTMAX};
+constexpr uint32_t kWg3Regs = kWideRegs[1];
+constexpr uint32_t kWideSoftmaxRegs = kWideRegs[2];
+static_assert(128 * kWideRegs[0] + 128 * kWideRegs[1] + 256 * kWideRegs[2] <= 65536, "wide K3 register split");
+template <int MODE>
+constexpr uint32_t kRoleRegs = kWideK3<MODE> ? kWideRegs[0] : 56;
 
 struct FaParams {
     int n, hq, rep, T_m, step;
@@ -372,7 +390,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
     };
 
     if (warp == 0) {
-        setmaxnreg_dec<56>();
+        setmaxnreg_dec<kRoleRegs<MODE>>();
         // ------------------------------------------------------------ producer
         // (the Q pair and the first contiguous K / V tile were issued at init)
         if (MODE == SPARSE) {
@@ -400,7 +418,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
             }
         }
     } else if (warp == 1) {
-        setmaxnreg_dec<56>();
+        setmaxnreg_dec<kRoleRegs<MODE>>();
         // ------------------------------------------------------------ MMA issuer
         if (ntiles > 0) {  // the whole warp runs the loop; one elected lane issues
             // SW128 descriptors: the high word (SBO 1024, version, layout) is a
@@ -477,7 +495,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
         }
         __syncwarp();
     } else if (warp < 4) {
-        setmaxnreg_dec<56>();  // warp 3: K3's V-row gathers; warps 2-3: K1's column sums
+        setmaxnreg_dec<kRoleRegs<MODE>>();  // warp 3: K3's V-row gathers; warps 2-3: K1's column sums
         if (MODE == SPARSE && warp == 3) gather_split(false, kWideK3<MODE> ? 1 : 3);
         if (MODE == SPARSE && kKGatherWarps == 2 && warp == 2) gather_split(true, 2);
         if (MODE == ANCHOR && P.qsum != nullptr && ntiles > 0) {
@@ -505,12 +523,12 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
             mbar_arrive(&S.bar_qsum);  // the epilogue reuses the Q tiles as staging
         }
     } else if (kWideK3<MODE> && warp >= 12) {
-        setmaxnreg_dec<40>();  // K3's fourth warpgroup: the second half of the V-row gathers
+        setmaxnreg_dec<kWg3Regs>();  // K3's fourth warpgroup: the second half of the V-row gathers
         // (warps 13-15 stay idle: more issuing / polling warps measured slower,
         // profiles/r2_experiments)
         if (warp == 12) gather_split(false, 2);
     } else {
-        if constexpr (kWideK3<MODE>) setmaxnreg_inc<208>();
+        if constexpr (kWideK3<MODE>) setmaxnreg_inc<kWideSoftmaxRegs>();
         else setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
