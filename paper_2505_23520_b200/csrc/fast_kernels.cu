@@ -65,6 +65,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define AA_K3_KGATHER_WARPS 2
 #endif
 constexpr int kKGatherWarps = AA_K3_KGATHER_WARPS;
+// softmax -> MMA hand-off arrivals per query tile: 128 (every thread) or 4
+// (one per warp after __syncwarp: measured 0.6-0.9% slower in K3)
+#ifndef AA_P_ARRIVALS
+#define AA_P_ARRIVALS 128
+#endif
+constexpr int kPArrivals = AA_P_ARRIVALS;
 // K3: warps issuing the V-row gathers (1: warp 3; 2: warps 3 and 12, one column
 // half each — the CTA then has a fourth warpgroup, warps 12-15, and the
 // softmax warpgroups 208 instead of 224 registers per thread)
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
             mbar_init(&S.bar_v_full[b], 1);
             mbar_init(&S.bar_v_empty[b], C);
             mbar_init(&S.bar_s_full[b], 1);
-            mbar_init(&S.bar_p_full[b], 128);
+            mbar_init(&S.bar_p_full[b], kPArrivals);
             mbar_init(&S.bar_o_done[b], 1);
         }
         fence_mbar_init();
@@ -532,6 +538,16 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
         else setmaxnreg_inc<224>();
         // ------------------------------------------------------------ softmax
         const int X = warp >= 8 ? 1 : 0;
+        // P_X (or S_X consumed) -> MMA warp: one arrival per warp (after every
+        // lane's own tcgen05.st / fence), or one per thread
+        auto arrive_p = [&](int x) {
+            if (kPArrivals == 4) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.bar_p_full[x]);
+            } else {
+                mbar_arrive(&S.bar_p_full[x]);
+            }
+        };
         const int nX = X ? nB : nA;
         const int qx = X ? qB : qA;
         if (X == 1 && !hasB) {
@@ -633,7 +649,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
                         rm = (acc2.x + acc2.y) / st.y;
                     }
                     tc_fence_before();
-                    mbar_arrive(&S.bar_p_full[X]);  // S consumed
+                    arrive_p(X);  // S consumed
 #pragma unroll
                     for (int sh = 16; sh; sh >>= 1) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
                     if (lane == 0) S.red[X][it & 1][quad] = rm;
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
                     l += la.x + la.y;
                     l_sel += ls.x + ls.y;
                     tc_fence_before();
-                    mbar_arrive(&S.bar_p_full[X]);
+                    arrive_p(X);
                     continue;
                 }
                 if (it == 0) {
@@ -722,7 +738,7 @@ __global__ void __launch_bounds__(kThreadsOf<MODE>, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 PROF(ps_comp += clock64() - ps_t1;)
-                mbar_arrive(&S.bar_p_full[X]);
+                arrive_p(X);
             }
             PROF(const long long t_epi0 = clock64();)
 
