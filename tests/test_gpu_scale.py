@@ -117,6 +117,13 @@ def test_qwen_128k_bench_heads(oracle):
     check_layer_heads(oracle, 131072, 28, 4, (0, 27))
 
 
+def test_ragged_130000_heads(oracle):
+    """A sequence length that leaves the last group partial (130,000 = 63
+    full groups + 976 rows): K3 runs its clusters with gather-only pairs
+    past the last query block — heads 4 and 30 against the oracle."""
+    check_layer_heads(oracle, 130000, 32, 8, (4, 30))
+
+
 def test_zero_anchor_arm_32k(oracle):
     """identify_stripes_zero_anchor (R/src/stripe_identify.cpp:90-95) on the
     fast path: anchor = 0 for every group, at 32k (heads of two KV groups)."""
